@@ -1,0 +1,368 @@
+"""Benchmark: packed-KV decode attention over the NSNQuant cache on B200.
+
+Headline workload (BASELINE.json configs[1]): LLaMA-3-8B attention shape --
+32 q-heads / 8 KV-heads (GQA 4), head_dim 128 -- 2-bit cache, batch 16,
+context 32K, one decode step = softmax(q.K^T/sqrt(d)).V for every (batch,
+q-head) over the packed pages.  Synthetic N(0,1) keys/values encoded by the
+product's own encode kernel; q N(0,1).
+
+metric  packed-KV decode attention GB/s: algorithmic bytes per step (the
+        reference bit ledger: 2292 B per 64-token K or V chunk in 2-bit,
+        vq.py:328-356, plus q in / out) / device time per step.
+value   whole job (all ranks), inputs resident in HBM.
+e2e     same metric through the public API (PagedKvCache.attend) with q
+        copied host->device and the output device->host inside the timing.
+
+``--impl reference`` times the CPU reference path instead (the C oracle, a
+restatement of the reference algorithm, on all host cores) on a bounded
+sample of the same workload.
+
+Multi-GPU: one process per GPU (torchrun); every rank holds its own batch
+of 16 sequences (weak scaling: the (batch, kv-head) units are independent,
+no collective inside attention); outputs are all-gathered over NCCL at the
+end of each step (the serving layout's only exchange).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+D, R = 128, 64
+LEDGER = {2: 2292, 1: 1268}
+CONFIGS = {
+    # name: (batch per rank, n_q_heads, n_kv_heads, context, bit_mode)
+    "c2": (16, 32, 8, 32768, 2),
+    "c2_1b": (16, 32, 8, 32768, 1),
+    "c1": (1, 8, 8, 4096, 1),
+}
+
+
+def step_bytes(B, Hq, Hkv, T, bit_mode) -> int:
+    """Algorithmic bytes of one decode step: every K and V
+    chunk's ledger bytes, the residual rows, q in (fp32) and out (fp32)."""
+    n_chunks = T // R
+    n_res = T - n_chunks * R
+    per_unit = n_chunks * LEDGER[bit_mode] * 2 + n_res * D * 4 * 2
+    return B * Hkv * per_unit + B * Hq * D * (4 + 4)
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            pass
+    return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def build_cache(cfg_name: str, device, seed: int):
+    """Encode a synthetic cache of the workload shape with the product's own
+    append path (chunked so fp32 staging stays small)."""
+    import torch
+
+    import paper_2505_18231_b200 as P
+
+    B, Hq, Hkv, T, bm = CONFIGS[cfg_name]
+    cb = P.default_codebook(f"{bm}b")
+    cfg = P.CacheConfig(d=D, bit_mode=cb.bit_mode)
+    cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, device=device,
+                           check_finite=False)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    block = 4096
+    done = 0
+    while done < T:
+        n = min(block, T - done)
+        k = torch.randn(B, Hkv, n, D, device=device, generator=gen)
+        v = torch.randn(B, Hkv, n, D, device=device, generator=gen)
+        cache.append(k, v)
+        done += n
+    torch.cuda.synchronize()
+    return cache
+
+
+def run_ours(args) -> dict | None:
+    import torch
+
+    import paper_2505_18231_b200 as P
+
+    world, rank, local = dist_setup()
+    device = torch.device("cuda", local)
+    B, Hq, Hkv, T, bm = CONFIGS[args.config]
+    cache = build_cache(args.config, device, seed=1234 + rank)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(99 + rank)
+    q = torch.randn(B, Hq, D, device=device, generator=gen)
+    out = torch.empty(B, Hq, D, device=device)
+    gathered = (torch.empty(world * B, Hq, D, device=device) if world > 1 else None)
+
+    def step():
+        cache.attend(q, out=out)
+        if gathered is not None:
+            torch.distributed.all_gather_into_tensor(gathered, out)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = P._lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = P._lib.launch_count() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    t_max = torch.tensor([ms], device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t_max, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t_max.item())
+    sbytes = step_bytes(B, Hq, Hkv, T, bm)
+    value = sbytes * world / (ms * 1e-3) / 1e9
+
+    # dominant kernel: time the attend launch alone (CUDA events on its stream)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record()
+    for _ in range(args.steps):
+        cache.attend(q, out=out)
+    k1.record()
+    torch.cuda.synchronize()
+    k_ms = k0.elapsed_time(k1) / args.steps
+
+    # e2e through the public API: pinned host q -> device, attend, out -> host
+    q_host = q.cpu().pin_memory()
+    out_host = torch.empty(B, Hq, D).pin_memory()
+    for _ in range(2):
+        out_host.copy_(cache.attend(q_host.to(device, non_blocking=True)), non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record()
+    for _ in range(args.steps):
+        qd = q_host.to(device, non_blocking=True)
+        out_host.copy_(cache.attend(qd), non_blocking=True)
+    x1.record()
+    torch.cuda.synchronize()
+    e2e_ms = x0.elapsed_time(x1) / args.steps
+    t2 = torch.tensor([e2e_ms], device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = float(t2.item())
+
+    peaks = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = sbytes / (k_ms * 1e-3) / 1e9
+    if rank != 0:
+        return None
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(args.config)
+        except Exception:
+            traffic = None
+    res = {
+        "metric": "packed-KV decode attention GB/s",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8 pages / fp32 accumulate",
+        "data": "synthetic N(0,1) K/V encoded by the product; N(0,1) q",
+        "config": {"workload": f"{args.config}: batch {B}/rank, {Hq}q/{Hkv}kv heads, d128, "
+                               f"context {T}, {bm}-bit",
+                   "global_batch": B * world, "seq_len": T, "parallelism": f"batch-sharded x{world}",
+                   "l2": "inputs larger than L2 (packed cache %.0f MB/rank)" % (sbytes / 1e6)},
+        "tokens_per_s": round(B * world / (ms * 1e-3), 1),
+        "e2e": {"value": round(sbytes * world / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                "h2d_bytes_per_step": B * Hq * D * 4, "d2h_bytes_per_step": B * Hq * D * 4,
+                "ms_per_step": round(e2e_ms, 4)},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("_fallback")
+                     else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                     "kernel": "nsnkv_decode_attend", "kernel_ms": round(k_ms, 4),
+                     "bytes_per_launch": sbytes},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
+    return res
+
+
+def cpu_baseline(cfg_name: str, budget_s: float = 15.0, threads: int | None = None) -> dict:
+    """The oracle (C restatement of the reference path) on the host cores:
+    encode a bounded sample of full-context (batch, kv-head) units, then time
+    attend_quantized-equivalent decode of all G q-heads of each unit."""
+    from oracle import oracle as orc
+
+    import paper_2505_18231_b200 as P
+
+    B, Hq, Hkv, T, bm = CONFIGS[cfg_name]
+    G = Hq // Hkv
+    cores = threads or os.cpu_count() or 1
+    cb = P.default_codebook(f"{bm}b")
+    n_chunks = T // R
+    # one unit's pages, replicated across the sample (decode cost is
+    # data-independent); encoded by the oracle itself
+    g = np.random.Generator(np.random.PCG64(7))
+    k = g.standard_normal((n_chunks, R, D), dtype=np.float32)
+    v = g.standard_normal((n_chunks, R, D), dtype=np.float32)
+    kw = orc.encode_many(k, True, cb.entries, bm, threads=cores)  # keys at pos 0 per chunk
+    vw = orc.encode_many(v, False, cb.entries, bm, threads=cores)
+    n_units = cores
+    kws = np.ascontiguousarray(np.broadcast_to(kw.reshape(1, -1), (n_units, kw.size)))
+    vws = np.ascontiguousarray(np.broadcast_to(vw.reshape(1, -1), (n_units, vw.size)))
+    q = g.standard_normal((n_units, G, D), dtype=np.float32)
+    t0 = time.perf_counter()
+    orc.attend_many(kws, vws, n_units, n_chunks, cb.entries, cb.entries, bm, q, threads=cores)
+    dt = time.perf_counter() - t0
+    unit_bytes = n_chunks * LEDGER[bm] * 2 + G * D * 8
+    return {"value": round(n_units * unit_bytes / dt / 1e9, 4), "unit": "GB/s", "cores": cores,
+            "kind": "port",
+            "sample": f"{n_units} full-context units x {G} q-heads ({T} tokens, {bm}-bit) "
+                      f"decoded in {dt:.2f}s on {cores} threads",
+            "seconds": round(dt, 3)}
+
+
+def run_reference(args) -> dict | None:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    B, Hq, Hkv, T, bm = CONFIGS[args.config]
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(args.config)
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(args.config))
+    best = vals[-1]
+    value = float(np.median([v["value"] for v in vals]))
+    return {
+        "impl": "reference", "metric": "packed-KV decode attention GB/s", "value": value,
+        "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8 pages / fp32 accumulate", "data": "synthetic N(0,1)",
+        "config": {"workload": f"{args.config}: batch {B}, {Hq}q/{Hkv}kv heads, d128, "
+                               f"context {T}, {bm}-bit", "global_batch": B, "seq_len": T},
+        "cpu_baseline": {**best, "value": value},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl != "reference":
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+// capi.cu -- C ABI glue: error state, launch accounting, codebook upload,
+// cache-view validation and the fused-attend dispatch.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "decode_common.cuh"
+
+using namespace nsnkv;
+
+struct nsnkv_codebook {
+  CodebookDev dev;
+};
+
+static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+extern "C" void nsnkv_internal_count_launch(int n) { g_launches += n; }
+
+extern "C" int nsnkv_internal_set_error(int code, const char *msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return code;
+}
+
+extern "C" int nsnkv_internal_check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return NSNKV_ERR_CUDA;
+  }
+  return NSNKV_OK;
+}
+
+extern "C" int nsnkv_version(void) { return 1; }
+extern "C" const char *nsnkv_last_error(void) { return g_err; }
+extern "C" int64_t nsnkv_launch_count(void) { return (int64_t)g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// codebook upload (codebook.py:71-106; kernels/__init__.py:44-51)
+// ---------------------------------------------------------------------------
+static inline uint32_t pack_half2(float a, float b) {
+  const __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+  return (uint32_t)__half_as_ushort(ha) | ((uint32_t)__half_as_ushort(hb) << 16);
+}
+
+extern "C" int nsnkv_codebook_create(const float *entries_host, const double *inv_norms_host,
+                                     int32_t bit_mode, nsnkv_codebook **out) {
+  if (!entries_host || !out) return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "codebook: null");
+  if (bit_mode != 1 && bit_mode != 2)
+    return nsnkv_internal_set_error(NSNKV_ERR_FORMAT, "codebook: bit_mode must be 1 or 2");
+  std::vector<double> inv(NENT);
+  std::vector<float> inv32(NENT);
+  for (int c = 0; c < NENT; ++c) {
+    const float *e = entries_host + 8 * c;
+    if (bit_mode == 2)
+      for (int k = 0; k < 8; ++k)
+        if (e[k] < 0.f)
+          return nsnkv_internal_set_error(NSNKV_ERR_FORMAT,
+                                          "two-bit codebook entries must be nonnegative");
+    if (inv_norms_host) {
+      inv[c] = inv_norms_host[c];
+    } else {  // component-order fp64 sum, kernels/__init__.py:47-51
+      double s = (double)e[0] * (double)e[0];
+      for (int k = 1; k < 8; ++k) s = s + (double)e[k] * (double)e[k];
+      if (s < 1e-24) return nsnkv_internal_set_error(NSNKV_ERR_FORMAT, "codebook contains a zero entry");
+      inv[c] = 1.0 / std::sqrt(s);
+    }
+    inv32[c] = (float)inv[c];
+  }
+  // decode gather tables: lane-private copies so a warp-wide gather never
+  // bank-conflicts (lane L reads word L of row idx)
+  std::vector<uint2> tk(NENT * 32), tv(NENT * 32);
+  for (int c = 0; c < NENT; ++c) {
+    const float *e = entries_host + 8 * c;
+    for (int L = 0; L < 32; ++L) {
+      for (int side = 0; side < 2; ++side) {
+        const int p = side == 0 ? (L & 3) : ((L >> 2) & 3);
+        const float a = e[2 * p], b = e[2 * p + 1];
+        const float ah = __half2float(__float2half_rn(a)), bh = __half2float(__float2half_rn(b));
+        uint2 v;
+        v.x = pack_half2(a, b);
+        v.y = pack_half2(a - ah, b - bh);
+        (side == 0 ? tk : tv)[c * 32 + L] = v;
+      }
+    }
+  }
+  nsnkv_codebook *cb = new nsnkv_codebook();
+  cb->dev.bit_mode = bit_mode;
+  cudaError_t err = cudaSuccess;
+  err = cudaMalloc(&cb->dev.entries, NENT * 8 * sizeof(float));
+  if (!err) err = cudaMalloc(&cb->dev.inv, NENT * sizeof(double));
+  if (!err) err = cudaMalloc(&cb->dev.inv32, NENT * sizeof(float));
+  if (!err) err = cudaMalloc(&cb->dev.tab_k, NENT * 32 * sizeof(uint2));
+  if (!err) err = cudaMalloc(&cb->dev.tab_v, NENT * 32 * sizeof(uint2));
+  if (!err) err = cudaMemcpy(cb->dev.entries, entries_host, NENT * 8 * sizeof(float), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(cb->dev.inv, inv.data(), NENT * sizeof(double), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(cb->dev.inv32, inv32.data(), NENT * sizeof(float), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(cb->dev.tab_k, tk.data(), NENT * 32 * sizeof(uint2), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(cb->dev.tab_v, tv.data(), NENT * 32 * sizeof(uint2), cudaMemcpyHostToDevice);
+  if (err) {
+    nsnkv_codebook_destroy(cb);
+    snprintf(g_err, sizeof(g_err), "codebook upload: %s", cudaGetErrorString(err));
+    return NSNKV_ERR_CUDA;
+  }
+  *out = cb;
+  return NSNKV_OK;
+}
+
+extern "C" int nsnkv_codebook_destroy(nsnkv_codebook *cb) {
+  if (!cb) return NSNKV_OK;
+  cudaFree(cb->dev.entries);
+  cudaFree(cb->dev.inv);
+  cudaFree(cb->dev.inv32);
+  cudaFree(cb->dev.tab_k);
+  cudaFree(cb->dev.tab_v);
+  delete cb;
+  return NSNKV_OK;
+}
+
+extern "C" int nsnkv_codebook_bit_mode(const nsnkv_codebook *cb) { return cb ? cb->dev.bit_mode : 0; }
+
+extern "C" int nsnkv_internal_codebook_dev(const nsnkv_codebook *cb, CodebookDev *out) {
+  if (!cb) return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "null codebook");
+  *out = cb->dev;
+  return NSNKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// cache view validation
+// ---------------------------------------------------------------------------
+int make_cache_view(const nsnkv_cache_view *in, CacheViewDev *out) {
+  if (!in) return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "null cache view");
+  if (!in->cb_k || !in->cb_v) return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "cache view: null codebook");
+  if (in->batch <= 0 || in->n_kv_heads <= 0 || in->n_q_heads <= 0 ||
+      in->n_q_heads % in->n_kv_heads != 0)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "cache view: bad head geometry");
+  if (in->max_tokens <= 0 || in->max_tokens % R != 0)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "cache view: max_tokens must be a positive multiple of 64");
+  if (in->cb_k->dev.bit_mode != in->cb_v->dev.bit_mode)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "codebook bit mode does not match chunk");
+  out->k_pool = in->k_pool;
+  out->v_pool = in->v_pool;
+  out->page_table = in->page_table;
+  out->page_table_stride = in->page_table_stride;
+  out->n_chunks = in->n_chunks;
+  out->k_res = in->k_res;
+  out->v_res = in->v_res;
+  out->n_res = in->n_res;
+  out->base_pos = in->base_pos;
+  out->batch = in->batch;
+  out->n_kv_heads = in->n_kv_heads;
+  out->n_q_heads = in->n_q_heads;
+  out->max_tokens = in->max_tokens;
+  out->rope_cs = reinterpret_cast<const float2 *>(in->rope_cs);
+  out->rope_pos0 = in->rope_pos0;
+  out->rope_n = in->rope_n;
+  out->cb_k = in->cb_k->dev;
+  out->cb_v = in->cb_v->dev;
+  return NSNKV_OK;
+}

@@ -1,0 +1,404 @@
+// encode.cu -- fused chunk flush: Normalize -> Shift -> Normalize, RoPE at
+// absolute positions (keys), fast Walsh-Hadamard transform (keys), exact
+// codebook search with the codebook in shared memory, scale adjustment,
+// 4-bit double quantization of s1 / o and bit-packing into one page.
+//
+// Reference (pkg/src/nsnkv): kvcache.py:114-154 (flush_chunk_keys/values),
+// nsn.py:58-85, core.py:50-66, rope.py:35-51, _native.pyx:16-38,
+// codebook.py:109-128, vq.py:74-93, vq.py:100-166, vq.py:211-279.
+//
+// One CTA (256 threads) per 64-token chunk.  All arithmetic that defines the
+// reference's outputs is reproduced operation by operation (IEEE fp32
+// divides, no FMA contraction where the reference rounds products, fp64 sums
+// in numpy's pairwise order), so pages are bit-identical to the oracle's.
+#include "common.cuh"
+#include "match.cuh"
+
+namespace nsnkv {
+
+constexpr int ENC_THREADS = 256;
+constexpr int XS = D + 4;  // padded smem row stride (floats)
+
+struct EncodeSmem {
+  float x[R][XS];                 // working rows
+  __align__(16) float ent[NENT * 8];
+  double inv[NENT];
+  float inv32[NENT];
+  float s1[R], s2[R], o[D];
+  double part[R];                 // per-token fp64 scratch
+  float s2adj[R];
+  uint8_t idx[R][NSUB];
+  uint8_t sgn[R][NSUB];
+  int cnt[NSNKV_NUM_COUNTERS];
+};
+
+// fp64 sum of squares of one token row held 4-per-lane (lane l owns
+// elements 4l..4l+3): lane partial ((a0+a1)+a2)+a3, then an xor butterfly
+// 16, 8, 4, 2, 1.  The oracle restates exactly this order.
+__device__ __forceinline__ double warp_row_sumsq(float4 v) {
+  double p = (double)v.x * (double)v.x;
+  p = __dadd_rn(p, (double)v.y * (double)v.y);
+  p = __dadd_rn(p, (double)v.z * (double)v.z);
+  p = __dadd_rn(p, (double)v.w * (double)v.w);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, off));
+  return p;
+}
+
+// _scale_per_token (nsn.py:58-65) on every row of s.x; returns clamps.
+__device__ int scale_rows(EncodeSmem &s, float *scale_out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float sqrt_d = 11.313708498984761f;  // float32(sqrt(128))
+  int clamps = 0;
+  for (int t = warp; t < R; t += ENC_THREADS / 32) {
+    float4 v = *reinterpret_cast<float4 *>(&s.x[t][4 * lane]);
+    const double ss = warp_row_sumsq(v);
+    const float nrm = __fsqrt_rn(__double2float_rn(ss));  // row_norms, core.py:50-53
+    float sc = __fdiv_rn(nrm, sqrt_d);
+    if (sc < 1e-8f) {  // NORM_EPS clamp, nsn.py:61-64
+      sc = 1e-8f;
+      ++clamps;
+    }
+    v.x = __fdiv_rn(v.x, sc);
+    v.y = __fdiv_rn(v.y, sc);
+    v.z = __fdiv_rn(v.z, sc);
+    v.w = __fdiv_rn(v.w, sc);
+    *reinterpret_cast<float4 *>(&s.x[t][4 * lane]) = v;
+    if (lane == 0) scale_out[t] = sc;
+  }
+  return lane == 0 ? clamps : 0;
+}
+
+// In-warp FWHT of one 128-row held 4-per-lane (fp32 add/sub only), then the
+// single orthonormal scale multiply (_native.pyx:24-37).
+__device__ __forceinline__ float4 warp_fwht128(float4 v) {
+  const int lane = threadIdx.x & 31;
+  // h = 1
+  float a = __fadd_rn(v.x, v.y), b = __fsub_rn(v.x, v.y);
+  float c = __fadd_rn(v.z, v.w), d = __fsub_rn(v.z, v.w);
+  // h = 2
+  v.x = __fadd_rn(a, c);
+  v.z = __fsub_rn(a, c);
+  v.y = __fadd_rn(b, d);
+  v.w = __fsub_rn(b, d);
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {  // h = 4m
+    const float ox = __shfl_xor_sync(0xffffffffu, v.x, m);
+    const float oy = __shfl_xor_sync(0xffffffffu, v.y, m);
+    const float oz = __shfl_xor_sync(0xffffffffu, v.z, m);
+    const float ow = __shfl_xor_sync(0xffffffffu, v.w, m);
+    if (lane & m) {  // this lane holds the "y" half
+      v.x = __fsub_rn(ox, v.x);
+      v.y = __fsub_rn(oy, v.y);
+      v.z = __fsub_rn(oz, v.z);
+      v.w = __fsub_rn(ow, v.w);
+    } else {
+      v.x = __fadd_rn(v.x, ox);
+      v.y = __fadd_rn(v.y, oy);
+      v.z = __fadd_rn(v.z, oz);
+      v.w = __fadd_rn(v.w, ow);
+    }
+  }
+  const float sc = 0.08838834764831845f;  // float32(1/sqrt(128))
+  v.x = __fmul_rn(v.x, sc);
+  v.y = __fmul_rn(v.y, sc);
+  v.z = __fmul_rn(v.z, sc);
+  v.w = __fmul_rn(v.w, sc);
+  return v;
+}
+
+// RTN-4 with f16 parameters (vq.py:100-117, 155-166) on n values held one
+// per thread of the first n threads of a group; lo/hi come in exact.
+__device__ __forceinline__ void rtn4_params(float lo, float hi, uint16_t &scale16,
+                                            uint16_t &zero16, float &scale32f, float &zero32f) {
+  const float sc = (hi == lo) ? 1.0f : __fdiv_rn(__fsub_rn(hi, lo), 15.0f);
+  scale16 = f32_to_f16_bits(sc);
+  zero16 = f32_to_f16_bits(lo);
+  scale32f = f16_bits_to_f32(scale16);
+  zero32f = f16_bits_to_f32(zero16);
+}
+
+__device__ __forceinline__ uint32_t rtn4_level(float v, float zero32f, float scale32f) {
+  float lv = rintf(__fdiv_rn(__fsub_rn(v, zero32f), scale32f));  // np.rint: half-even
+  if (!(lv == lv)) lv = 0.f;  // NaN (scale16 == 0): the reference leaves this undefined
+  lv = fminf(fmaxf(lv, 0.f), 15.f);
+  return (uint32_t)lv;
+}
+
+__global__ void __launch_bounds__(ENC_THREADS) encode_chunks_kernel(
+    const float *__restrict__ residual, int n_resid, const void *__restrict__ fresh, int fresh_bf16,
+    int64_t n_fresh, int n_flush, int is_key, const int64_t *__restrict__ start_pos,
+    const float2 *__restrict__ rope_cs, int64_t rope_pos0, int64_t rope_n, CodebookDev cb,
+    int strategy, uint8_t *__restrict__ pool, const int32_t *__restrict__ page_ids,
+    int page_id_stride, int32_t *__restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EncodeSmem &s = *reinterpret_cast<EncodeSmem *>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int u = blockIdx.x / n_flush;
+  const int k = blockIdx.x - u * n_flush;
+  const PageLayout L = page_layout(cb.bit_mode);
+  const bool fold = cb.bit_mode == 2;
+
+  if (tid < NSNKV_NUM_COUNTERS) s.cnt[tid] = 0;
+  for (int i = tid; i < NENT * 8; i += ENC_THREADS) s.ent[i] = cb.entries[i];
+  for (int i = tid; i < NENT; i += ENC_THREADS) {
+    s.inv[i] = cb.inv[i];
+    s.inv32[i] = cb.inv32[i];
+  }
+  // ---- 1. gather the chunk's 64 stream rows (kvcache.py:179-186) ----------
+  for (int i = tid; i < R * (D / 4); i += ENC_THREADS) {
+    const int t = i / (D / 4), c4 = i - t * (D / 4);
+    const int64_t srow = (int64_t)k * R + t;
+    float4 v;
+    if (srow < n_resid) {
+      v = *reinterpret_cast<const float4 *>(residual + ((int64_t)u * R + srow) * D + 4 * c4);
+    } else {
+      const int64_t fr = (int64_t)u * n_fresh + (srow - n_resid);
+      if (fresh_bf16) {
+        const uint2 raw =
+            *reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(fresh) + fr * D + 4 * c4);
+        v.x = bf16_to_f32((uint16_t)(raw.x & 0xffffu));
+        v.y = bf16_to_f32((uint16_t)(raw.x >> 16));
+        v.z = bf16_to_f32((uint16_t)(raw.y & 0xffffu));
+        v.w = bf16_to_f32((uint16_t)(raw.y >> 16));
+      } else {
+        v = *reinterpret_cast<const float4 *>(static_cast<const float *>(fresh) + fr * D + 4 * c4);
+      }
+    }
+    *reinterpret_cast<float4 *>(&s.x[t][4 * c4]) = v;
+  }
+  __syncthreads();
+
+  // ---- 2. nsn_forward (nsn.py:68-85) --------------------------------------
+  int clamps = scale_rows(s, s.s1);
+  __syncthreads();
+  if (tid < D) {  // col_means: fp64 sequential sum over tokens / n (core.py:56-66)
+    double acc = 0.0;
+    for (int t = 0; t < R; ++t) acc = __dadd_rn(acc, (double)s.x[t][tid]);
+    s.o[tid] = __double2float_rn(__ddiv_rn(acc, (double)R));
+  }
+  __syncthreads();
+  for (int i = tid; i < R * D; i += ENC_THREADS) {
+    const int t = i / D, c = i - t * D;
+    s.x[t][c] = __fsub_rn(s.x[t][c], s.o[c]);
+  }
+  __syncthreads();
+  clamps += scale_rows(s, s.s2);
+  __syncthreads();
+
+  // ---- 3. keys: RoPE at absolute positions, then FWHT (kvcache.py:121-123)
+  if (is_key) {
+    const int64_t pos_base = start_pos[u] + (int64_t)k * R;
+    for (int t = warp; t < R; t += ENC_THREADS / 32) {
+      int64_t row = pos_base + t - rope_pos0;
+      row = row < 0 ? 0 : (row >= rope_n ? rope_n - 1 : row);
+      float4 v = *reinterpret_cast<float4 *>(&s.x[t][4 * lane]);
+      const float4 cs = *reinterpret_cast<const float4 *>(&rope_cs[row * NPAIR + 2 * lane]);
+      // pair j = 2*lane: (v.x, v.y) ; pair j+1: (v.z, v.w); rope.py:49-50
+      float4 r;
+      r.x = __fsub_rn(__fmul_rn(v.x, cs.x), __fmul_rn(v.y, cs.y));
+      r.y = __fadd_rn(__fmul_rn(v.x, cs.y), __fmul_rn(v.y, cs.x));
+      r.z = __fsub_rn(__fmul_rn(v.z, cs.z), __fmul_rn(v.w, cs.w));
+      r.w = __fadd_rn(__fmul_rn(v.z, cs.w), __fmul_rn(v.w, cs.z));
+      r = warp_fwht128(r);
+      *reinterpret_cast<float4 *>(&s.x[t][4 * lane]) = r;
+    }
+    __syncthreads();
+  }
+
+  // ---- 4. codebook match (codebook.py:109-128, _native.pyx:41-87) -------
+  {
+    const int t = tid >> 2;          // token
+    const int j0 = (tid & 3) * 4;    // first of 4 sub-vectors
+    float u4[4][8];
+    uint32_t sb[4];
+    bool zero[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float v[8];
+      const float4 a = *reinterpret_cast<float4 *>(&s.x[t][8 * (j0 + i)]);
+      const float4 b = *reinterpret_cast<float4 *>(&s.x[t][8 * (j0 + i) + 4]);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      zero[i] = sq_norm8_pairwise(v) < 1e-24;
+      sb[i] = fold_signs(v, u4[i], fold);
+    }
+    int best[4];
+    const uint32_t slow =
+        match_multi<4>(u4, reinterpret_cast<const float4 *>(s.ent), s.inv32, s.ent, s.inv, best);
+    int nz = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      s.idx[t][j0 + i] = zero[i] ? 0 : (uint8_t)best[i];
+      s.sgn[t][j0 + i] = zero[i] ? 0 : (uint8_t)sb[i];
+      nz += zero[i] ? 1 : 0;
+    }
+    if (nz) atomicAdd(&s.cnt[NSNKV_CNT_ZERO], nz);
+    if (slow) atomicAdd(&s.cnt[NSNKV_CNT_NEARTIE], __popc(slow));
+  }
+  if (clamps) atomicAdd(&s.cnt[NSNKV_CNT_CLAMP], clamps);
+  __syncthreads();
+
+  // ---- 5. scale adjustment (vq.py:74-93, 249-254) --------------------------
+  {
+    // 4 tokens per warp pass; lane = 8 * token_slot + accumulator j.
+    const int slot = lane >> 3, j = lane & 7;
+    for (int t0 = warp * 4; t0 < R; t0 += (ENC_THREADS / 32) * 4) {
+      const int t = t0 + slot;
+      double v2 = 0.0, q2 = 0.0, dt = 0.0;
+#pragma unroll 4
+      for (int i = 0; i < NSUB; ++i) {  // element 8i + j; numpy pairwise_sum order
+        const float v = s.x[t][8 * i + j];
+        float c = s.ent[s.idx[t][i] * 8 + j];
+        if (fold && ((s.sgn[t][i] >> j) & 1)) c = -c;  // _SIGN_LUT, codebook.py:49
+        const double vd = (double)v, cd = (double)c;
+        if (i == 0) {
+          v2 = vd * vd; q2 = cd * cd; dt = vd * cd;
+        } else {
+          v2 = __dadd_rn(v2, vd * vd);
+          q2 = __dadd_rn(q2, cd * cd);
+          dt = __dadd_rn(dt, vd * cd);
+        }
+      }
+#pragma unroll
+      for (int off = 1; off <= 4; off <<= 1) {
+        v2 = __dadd_rn(v2, __shfl_xor_sync(0xffffffffu, v2, off));
+        q2 = __dadd_rn(q2, __shfl_xor_sync(0xffffffffu, q2, off));
+        dt = __dadd_rn(dt, __shfl_xor_sync(0xffffffffu, dt, off));
+      }
+      if (j == 0) {
+        double f = 1.0;
+        int fb = 0;
+        if (strategy == NSNKV_STRATEGY_MIN_L2) {
+          f = __ddiv_rn(dt, q2);
+        } else if (strategy == NSNKV_STRATEGY_NORM_MATCH) {
+          f = __dsqrt_rn(__ddiv_rn(v2, q2));
+        } else if (strategy == NSNKV_STRATEGY_PARALLEL) {
+          const bool bad = fabs(dt) <= __dmul_rn(1e-10, __dsqrt_rn(__dmul_rn(v2, q2)));
+          f = bad ? __dsqrt_rn(__ddiv_rn(v2, q2)) : __ddiv_rn(v2, dt);
+          fb = bad ? 1 : 0;
+        }
+        s.s2adj[t] = __double2float_rn(__dmul_rn((double)s.s2[t], f));
+        if (fb) atomicAdd(&s.cnt[NSNKV_CNT_FALLBACK], 1);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 6. pack the page ----------------------------------------------------
+  uint8_t *page = pool + (int64_t)page_ids[(int64_t)u * page_id_stride + k] * L.bytes;
+  // indices: 1024 bytes, 4 per thread
+  {
+    const uint32_t w = *reinterpret_cast<const uint32_t *>(&s.idx[0][0] + 4 * tid);
+    *reinterpret_cast<uint32_t *>(page + L.idx + 4 * tid) = w;
+  }
+  if (fold) {  // bit-permuted signs: word p of token t
+    const int t = tid >> 2, p = tid & 3;
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < NSUB; ++j) {
+      const uint32_t b = s.sgn[t][j];
+      w |= ((b >> (2 * p)) & 1u) << j;
+      w |= ((b >> (2 * p + 1)) & 1u) << (16 + j);
+    }
+    *reinterpret_cast<uint32_t *>(page + L.sgn + 4 * tid) = w;
+  }
+  // s2 (f16, vq.py:259), s1 and o double quantization (vq.py:257-258)
+  if (warp == 0) {
+    // s1: one group of 64 values; lane holds tokens lane and lane + 32
+    const float a = s.s1[lane], b = s.s1[lane + 32];
+    float lo = fminf(a, b), hi = fmaxf(a, b);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+    }
+    uint16_t sc16, z16;
+    float sc32, z32;
+    rtn4_params(lo, hi, sc16, z16, sc32, z32);
+    const uint32_t la = rtn4_level(a, z32, sc32), lb = rtn4_level(b, z32, sc32);
+    // nibble pairs: byte i = level[2i] | level[2i+1] << 4
+    const uint32_t la_next = __shfl_down_sync(0xffffffffu, la, 1);
+    const uint32_t lb_next = __shfl_down_sync(0xffffffffu, lb, 1);
+    if ((lane & 1) == 0) {
+      page[L.s1n + lane / 2] = (uint8_t)(la | (la_next << 4));
+      page[L.s1n + 16 + lane / 2] = (uint8_t)(lb | (lb_next << 4));
+    }
+    if (lane == 0) {
+      uint16_t *par = reinterpret_cast<uint16_t *>(page + L.par);
+      par[0] = sc16;
+      par[1] = z16;
+    }
+  } else if (warp >= 1 && warp <= 4) {
+    // o: group g = warp - 1 covers channels 32g .. 32g+31
+    const int g = warp - 1;
+    const float v = s.o[32 * g + lane];
+    float lo = v, hi = v;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+    }
+    uint16_t sc16, z16;
+    float sc32, z32;
+    rtn4_params(lo, hi, sc16, z16, sc32, z32);
+    const uint32_t lv = rtn4_level(v, z32, sc32);
+    const uint32_t lv_next = __shfl_down_sync(0xffffffffu, lv, 1);
+    if ((lane & 1) == 0) page[L.on + 16 * g + lane / 2] = (uint8_t)(lv | (lv_next << 4));
+    if (lane == 0) {
+      uint16_t *par = reinterpret_cast<uint16_t *>(page + L.par);
+      par[2 + g] = sc16;
+      par[6 + g] = z16;
+    }
+  } else if (warp == 5) {
+    uint16_t *s2p = reinterpret_cast<uint16_t *>(page + L.s2);
+    s2p[lane] = f32_to_f16_bits(s.s2adj[lane]);
+    s2p[lane + 32] = f32_to_f16_bits(s.s2adj[lane + 32]);
+  } else if (warp == 6) {
+    // zero the page padding so pages are deterministic byte images
+    for (int i = L.ledger + lane; i < L.bytes; i += 32) page[i] = 0;
+  }
+  if (counters && tid < NSNKV_NUM_COUNTERS)
+    counters[(int64_t)blockIdx.x * NSNKV_NUM_COUNTERS + tid] = s.cnt[tid];
+}
+
+}  // namespace nsnkv
+
+using namespace nsnkv;
+
+extern "C" int nsnkv_internal_codebook_dev(const nsnkv_codebook *cb, CodebookDev *out);
+
+extern "C" int nsnkv_encode_chunks(const float *residual, int32_t n_resid, const void *fresh,
+                                   int32_t fresh_bf16, int64_t n_fresh, int32_t n_units,
+                                   int32_t n_flush, int32_t is_key, const int64_t *start_pos,
+                                   const float *rope_cs, int64_t rope_pos0, int64_t rope_n,
+                                   const nsnkv_codebook *cb, int32_t strategy, uint8_t *pool,
+                                   const int32_t *page_ids, int32_t page_id_stride,
+                                   int32_t *counters, void *stream) {
+  if (n_units < 0 || n_flush < 0 || n_resid < 0 || n_resid > R || n_fresh < 0)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "encode_chunks: bad sizes");
+  if ((int64_t)n_flush * R > (int64_t)n_resid + n_fresh)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "encode_chunks: not enough rows to flush");
+  if (strategy < 0 || strategy > 3)
+    return nsnkv_internal_set_error(NSNKV_ERR_UNSUPPORTED, "encode_chunks: unknown strategy");
+  if ((int64_t)n_units * n_flush == 0) return NSNKV_OK;
+  if (is_key && (!rope_cs || rope_n <= 0))
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "encode_chunks: keys need a RoPE table");
+  CodebookDev dev;
+  int rc = nsnkv_internal_codebook_dev(cb, &dev);
+  if (rc) return rc;
+  const size_t smem = sizeof(EncodeSmem);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(encode_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_set = true;
+  }
+  const int64_t blocks = (int64_t)n_units * n_flush;
+  encode_chunks_kernel<<<(unsigned)blocks, ENC_THREADS, smem, (cudaStream_t)stream>>>(
+      residual, n_resid, fresh, fresh_bf16, n_fresh, n_flush, is_key, start_pos,
+      reinterpret_cast<const float2 *>(rope_cs), rope_pos0, rope_n, dev, strategy, pool, page_ids,
+      page_id_stride, counters);
+  nsnkv_internal_count_launch(1);
+  return nsnkv_internal_check_launch("encode_chunks");
+}
