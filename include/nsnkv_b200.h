@@ -173,6 +173,11 @@ typedef struct nsnkv_cache_view {
   int64_t rope_n;
   const nsnkv_codebook *cb_k;
   const nsnkv_codebook *cb_v;
+  int64_t total_chunks;      /* sum of n_chunks (host copy), or -1 to let
+                                the library read it back (synchronises)   */
+  int32_t fast_fp16;         /* 0: codewords as fp16 hi + lo (~22-bit, the
+                                default); 1: plain fp16 codewords (faster,
+                                ~5e-4 relative output error on 2-bit)     */
 } nsnkv_cache_view;
 
 /* Raw q.K^T of every cached token (quantized chunks first, then residual),

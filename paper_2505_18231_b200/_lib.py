@@ -61,6 +61,8 @@ class CacheView(ctypes.Structure):
         ("rope_n", c_i64),
         ("cb_k", c_void_p),
         ("cb_v", c_void_p),
+        ("total_chunks", c_i64),
+        ("fast_fp16", c_int),
     ]
 
 

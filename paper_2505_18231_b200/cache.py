@@ -141,9 +141,13 @@ class PagedKvCache:
 
     def __init__(self, config: CacheConfig, batch: int, n_kv_heads: int, max_tokens: int = 0,
                  cb_k: Codebook | None = None, cb_v: Codebook | None = None,
-                 base_position: int = 0, device=None, check_finite: bool = True):
+                 base_position: int = 0, device=None, check_finite: bool = True,
+                 fast_fp16: bool = False):
         config.check_gpu_path()
         self.check_finite = check_finite
+        # decode precision: False = codewords as fp16 hi + lo (~22 bits, the
+        # default); True = plain fp16 codewords (faster, ~5e-4 relative error)
+        self.fast_fp16 = bool(fast_fp16)
         if batch < 1 or n_kv_heads < 1:
             raise ShapeMismatch("batch and n_kv_heads must be >= 1")
         self.config = config
@@ -312,6 +316,8 @@ class PagedKvCache:
         cv.rope_n = table.shape[0]
         cv.cb_k = cb_k.device_handle(self.device)
         cv.cb_v = cb_v.device_handle(self.device)
+        cv.total_chunks = self.units * self.n_chunks
+        cv.fast_fp16 = 1 if self.fast_fp16 else 0
         return cv
 
     def _q(self, q) -> torch.Tensor:
@@ -413,13 +419,16 @@ _LAYOUT = {  # idx, sgn, s2, s1n, on, par
 
 
 def unpermute_signs(words: np.ndarray) -> np.ndarray:
-    """[64, 4] u32 decode-order sign words -> natural sign bytes [64, 16]."""
+    """[64, 4] u32 decode-order sign words -> natural sign bytes [64, 16].
+    Word q of a token covers subs 4q+m; bit 4m+p holds the sign of component
+    2p and bit 16+4m+p the sign of component 2p+1 (see csrc/common.cuh)."""
     w = words.astype(np.uint32)
-    j = np.arange(16, dtype=np.uint32)
     out = np.zeros((w.shape[0], 16), np.uint32)
-    for p in range(4):
-        out |= ((w[:, p:p + 1] >> j) & 1) << (2 * p)
-        out |= ((w[:, p:p + 1] >> (16 + j)) & 1) << (2 * p + 1)
+    for q in range(4):
+        for m in range(4):
+            for p in range(4):
+                out[:, 4 * q + m] |= ((w[:, q] >> (4 * m + p)) & 1) << (2 * p)
+                out[:, 4 * q + m] |= ((w[:, q] >> (16 + 4 * m + p)) & 1) << (2 * p + 1)
     return out.astype(np.uint8)
 
 
@@ -427,10 +436,11 @@ def permute_signs(signs: np.ndarray) -> np.ndarray:
     """Natural sign bytes [64, 16] -> decode-order words [64, 4] u32."""
     s = signs.astype(np.uint32)
     words = np.zeros((s.shape[0], 4), np.uint32)
-    for p in range(4):
-        for j in range(16):
-            words[:, p] |= ((s[:, j] >> (2 * p)) & 1) << j
-            words[:, p] |= ((s[:, j] >> (2 * p + 1)) & 1) << (16 + j)
+    for q in range(4):
+        for m in range(4):
+            for p in range(4):
+                words[:, q] |= ((s[:, 4 * q + m] >> (2 * p)) & 1) << (4 * m + p)
+                words[:, q] |= ((s[:, 4 * q + m] >> (2 * p + 1)) & 1) << (16 + 4 * m + p)
     return words
 
 

@@ -70,21 +70,20 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
     }
     inv32[c] = (float)inv[c];
   }
-  // decode gather tables: lane-private copies so a warp-wide gather never
-  // bank-conflicts (lane L reads word L of row idx)
-  std::vector<uint2> tk(NENT * 32), tv(NENT * 32);
+  // decode gather table: row c = [hi codeword x 8 slots][lo codeword x 8 slots]
+  std::vector<uint4> tw(NENT * 16);
   for (int c = 0; c < NENT; ++c) {
     const float *e = entries_host + 8 * c;
-    for (int L = 0; L < 32; ++L) {
-      for (int side = 0; side < 2; ++side) {
-        const int p = side == 0 ? (L & 3) : ((L >> 2) & 3);
-        const float a = e[2 * p], b = e[2 * p + 1];
-        const float ah = __half2float(__float2half_rn(a)), bh = __half2float(__float2half_rn(b));
-        uint2 v;
-        v.x = pack_half2(a, b);
-        v.y = pack_half2(a - ah, b - bh);
-        (side == 0 ? tk : tv)[c * 32 + L] = v;
-      }
+    uint32_t hw[4], lw[4];
+    for (int p = 0; p < 4; ++p) {
+      const float a = e[2 * p], b = e[2 * p + 1];
+      const float ah = __half2float(__float2half_rn(a)), bh = __half2float(__float2half_rn(b));
+      hw[p] = pack_half2(a, b);
+      lw[p] = pack_half2(a - ah, b - bh);
+    }
+    for (int slot = 0; slot < 8; ++slot) {
+      tw[c * 16 + slot] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      tw[c * 16 + 8 + slot] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
   }
   nsnkv_codebook *cb = new nsnkv_codebook();
@@ -93,13 +92,11 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
   err = cudaMalloc(&cb->dev.entries, NENT * 8 * sizeof(float));
   if (!err) err = cudaMalloc(&cb->dev.inv, NENT * sizeof(double));
   if (!err) err = cudaMalloc(&cb->dev.inv32, NENT * sizeof(float));
-  if (!err) err = cudaMalloc(&cb->dev.tab_k, NENT * 32 * sizeof(uint2));
-  if (!err) err = cudaMalloc(&cb->dev.tab_v, NENT * 32 * sizeof(uint2));
+  if (!err) err = cudaMalloc(&cb->dev.tabw, NENT * 16 * sizeof(uint4));
   if (!err) err = cudaMemcpy(cb->dev.entries, entries_host, NENT * 8 * sizeof(float), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(cb->dev.inv, inv.data(), NENT * sizeof(double), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(cb->dev.inv32, inv32.data(), NENT * sizeof(float), cudaMemcpyHostToDevice);
-  if (!err) err = cudaMemcpy(cb->dev.tab_k, tk.data(), NENT * 32 * sizeof(uint2), cudaMemcpyHostToDevice);
-  if (!err) err = cudaMemcpy(cb->dev.tab_v, tv.data(), NENT * 32 * sizeof(uint2), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(cb->dev.tabw, tw.data(), NENT * 16 * sizeof(uint4), cudaMemcpyHostToDevice);
   if (err) {
     nsnkv_codebook_destroy(cb);
     snprintf(g_err, sizeof(g_err), "codebook upload: %s", cudaGetErrorString(err));
@@ -114,8 +111,7 @@ extern "C" int nsnkv_codebook_destroy(nsnkv_codebook *cb) {
   cudaFree(cb->dev.entries);
   cudaFree(cb->dev.inv);
   cudaFree(cb->dev.inv32);
-  cudaFree(cb->dev.tab_k);
-  cudaFree(cb->dev.tab_v);
+  cudaFree(cb->dev.tabw);
   delete cb;
   return NSNKV_OK;
 }
@@ -159,5 +155,7 @@ int make_cache_view(const nsnkv_cache_view *in, CacheViewDev *out) {
   out->rope_n = in->rope_n;
   out->cb_k = in->cb_k->dev;
   out->cb_v = in->cb_v->dev;
+  out->total_chunks = in->total_chunks;
+  out->fast_fp16 = in->fast_fp16;
   return NSNKV_OK;
 }

@@ -24,8 +24,9 @@ constexpr int NENT = 256;               // codebook entries
 //   [IDX]   u8  idx[64][16]          payload index per (token, sub-vector)
 //   [SGN]   u32 sgn[64][4]           2-bit mode only; 128 sign bits per token,
 //                                    bit-permuted for the decode fragments:
-//                                    word p, bit j      = sign bit 2p   of sub j
-//                                    word p, bit 16 + j = sign bit 2p+1 of sub j
+//                                    word q covers subs 4q+m (m = 0..3);
+//                                    bit 4m+p      = sign bit 2p   of sub 4q+m
+//                                    bit 16+4m+p   = sign bit 2p+1 of sub 4q+m
 //   [S2]    f16 s2[64]               adjusted second scale (vq.py:254-259)
 //   [S1N]   u8  s1 nibbles[32]       RTN-4 levels of s1, low nibble first
 //   [ON]    u8  o nibbles[64]        RTN-4 levels of o, low nibble first
@@ -48,10 +49,11 @@ struct CodebookDev {
   float *entries;      // [256][8] fp32 (codebook.py active_entries)
   double *inv;         // [256] fp64 1/||e|| (kernels/__init__.py:44-51)
   float *inv32;        // [256] fp32 copy for the pre-pass
-  // decode gather tables: per (entry, lane) the lane's component pair as
-  // (hi half2, lo half2) with hi = fp16(e), lo = fp16(e - hi).
-  uint2 *tab_k;        // [256][32] lane L owns pair L % 4   (score side)
-  uint2 *tab_v;        // [256][32] lane L owns pair (L/4)%4 (value side)
+  // decode gather table (64 KB): row c = 256 bytes = [hi x 8 slots][lo x 8
+  // slots], each slot the whole codeword as 8 fp16 (hi = fp16(e),
+  // lo = fp16(e - hi)); 8 replicas so a quarter-warp of 16-byte loads with
+  // slot = lane % 8 never bank-conflicts.
+  uint4 *tabw;
   int bit_mode;
 };
 

@@ -1,60 +1,855 @@
-// decode_attend.cu -- nsnkv_decode_attend (attention.py:136-142).
-// v0: scores -> fp64 softmax -> weighted output, through the unfused kernels
-// of decode_ref.cu.  Replaced by the split-K flash-decoding kernel.
+// decode_attend.cu -- nsnkv_decode_attend: fused split-K flash-decoding over
+// the packed cache (reference attention.py:83-142 in one pass).
+//
+// Per (unit = batch x kv-head, 64-token chunk) the kernel computes, for the G
+// q-heads of the GQA group,
+//   score_t = s1_t * ( s2_t * <HT(q), c_t> + <q, RoPE(o, p0 + tau)> )
+//   out     = FWHT( sum_t softmax_t * s1_t * (s2_t * c'_t + o') )
+// with c_t / c'_t the sign-applied codewords of the key / value payload.
+//
+// Engine:
+//  * persistent CTAs, one per SM, stream-K split of the global chunk list;
+//  * a producer warp streams each chunk's K page, V page and RoPE row p0 into
+//    a 4-stage shared-memory ring with 1-D TMA bulk copies (cp.async.bulk +
+//    mbarrier complete_tx);
+//  * 4 consumer warps each own 16 of the chunk's 64 tokens;
+//  * codewords are gathered from lane-private shared-memory tables (one
+//    8-byte word per (entry, lane): the lane's component pair as fp16 hi and
+//    fp16 lo halves -- conflict-free, ~22-bit precision) and fed to legacy
+//    mma.sync m16n8k16 (fp16 in, fp32 accumulate):
+//      K side:  D[token][head] += codewords[token][ch] . HT(q)[ch][head]
+//      shift :  D[token][head] += Tab[tau][(cos,sin)_j] . AB[(cos,sin)_j][head]
+//               (angle addition: <q,RoPE(o,p0+tau)> = sum_j a_j cos(tau f_j)
+//                + b_j sin(tau f_j), a/b from q and RoPE(o, p0))
+//      V side:  D[ch][head] += codewords^T[ch][token] . P'[token][head]
+//    q and P' are split hi/lo across the two columns of each head, so every
+//    product carries ~22 bits;
+//  * online softmax (base-2) per warp, merged across warps / CTAs by
+//    nsnkv_decode_combine together with the exact residual rows, then one
+//    inverse FWHT per (batch, q-head).
 #include "common.cuh"
 #include "decode_common.cuh"
 
 namespace nsnkv {
 
-// softmax_rows (attention.py:46-50) on scores / sqrt(d), fp64, in place
-// (fp32 result).  One CTA per (batch, q-head) row.
-__global__ void __launch_bounds__(256) softmax_kernel(CacheViewDev cv, float *__restrict__ sw,
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// x ^ (w & 0x80008000): flip the fp16 sign bits selected by bits 15 / 31 of w
+// in one LOP3
+__device__ __forceinline__ uint32_t xor_sign(uint32_t x, uint32_t w) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(r) : "r"(x), "r"(w), "r"(0x80008000u));
+  return r;
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo16, float hi16) {
+  const __half2 h = __floats2half2_rn(lo16, hi16);
+  return *reinterpret_cast<const uint32_t *>(&h);
+}
+// x = hi + lo with hi = fp16(x), lo = fp16(x - hi)
+__device__ __forceinline__ void split_h(float x, float &hi, float &lo) {
+  hi = __half2float(__float2half_rn(x));
+  lo = x - hi;
+}
+
+// ---------------------------------------------------------------------------
+// configuration
+// ---------------------------------------------------------------------------
+constexpr int ROPE_ROW_BYTES = NPAIR * 8;        // 64 x (cos, sin) fp32
+constexpr int STAGE_BYTES = 2 * NSNKV_PAGE_BYTES_2B + ROPE_ROW_BYTES;
+constexpr int ATT_SMEM_BYTES = 196608;           // two 64 KB-aligned tables + misc
+constexpr int MISC_MAX = 65536 - 1024;           // below the tables (1 KB is reserved)
+constexpr float LOG2E_OVER_SQRTD = 1.4426950408889634f * 0.08838834764831845f;
+
+template <int G>
+struct AttCfg {
+  static constexpr int NT = (2 * G + 7) / 8;  // n-tiles of 8 (head, hi/lo) columns
+  static constexpr int NGRP = 2;               // consumer groups of 4 warps
+  static constexpr int THREADS = 4 * NGRP * 32;
+  static constexpr int NSTAGE = G <= 4 ? 8 : 4; // page ring depth
+};
+
+// Per-group prologue / merge scratch.  The unit-merge buffers alias the
+// per-chunk buffers (a flush never overlaps a chunk).
+template <int G>
+struct AttGroup {
+  static constexpr int NT = AttCfg<G>::NT;
+  struct Chunk {
+    uint2 ab[2][NT][8][32];   // o-term B fragments, double-buffered per chunk
+    float ov[2][D];           // dequantized value shift vector
+    float4 sc[2][R];          // (s1k*s2k, s1k, s1v*s2v, s1v) per token
+    float qh[G][D];           // HT(q) (unit set-up only)
+  };
+  struct Merge {
+    float mrg[4][G][D];       // per-warp partials for the unit merge
+    float ml[4][G][2];
+  };
+  union {
+    Chunk ck;
+    Merge mg;
+  };
+  float q[G][D];              // RoPE'd q of the group's current unit
+};
+
+// Everything but the tables: stage ring, barriers and the two groups'
+// scratch (below the 64 KB-aligned tables).
+template <int G>
+struct AttMisc {
+  static constexpr int NSTAGE = AttCfg<G>::NSTAGE;
+  __align__(128) uint8_t st[NSTAGE][STAGE_BYTES];
+  AttGroup<G> grp[AttCfg<G>::NGRP];
+  uint64_t full[NSTAGE];
+  uint64_t pro[AttCfg<G>::NGRP][2];   // per-group prologue barriers (2 slots)
+  uint64_t tabs;
+};
+
+struct ChunkCursor {
+  int u, c, n;  // unit, chunk within unit, chunks of the unit
+};
+
+__device__ __forceinline__ void cursor_advance(ChunkCursor &cur, const int32_t *n_chunks,
+                                               int n_units) {
+  if (++cur.c >= cur.n) {
+    cur.c = 0;
+    cur.n = 0;
+    while (cur.n == 0 && ++cur.u < n_units) cur.n = n_chunks[cur.u];
+  }
+}
+
+// Warp-parallel seek of global chunk x (all 32 lanes call; every lane gets
+// the result).  Units with zero chunks are skipped.
+__device__ __forceinline__ ChunkCursor cursor_seek(int64_t x, const int32_t *n_chunks,
+                                                   int n_units) {
+  const int lane = threadIdx.x & 31;
+  int64_t acc = 0;
+  for (int base = 0; base < n_units; base += 32) {
+    const int u = base + lane;
+    const int64_t n = u < n_units ? n_chunks[u] : 0;
+    int64_t incl = n;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, n > 0 && acc + incl > x);
+    if (hit) {
+      const int L = __ffs(hit) - 1;
+      const int64_t excl = __shfl_sync(0xffffffffu, incl - n, L);
+      const int nn = (int)__shfl_sync(0xffffffffu, n, L);
+      return ChunkCursor{base + L, (int)(x - acc - excl), nn};
+    }
+    acc += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return ChunkCursor{n_units, 0, 0};
+}
+
+__host__ __device__ __forceinline__ int64_t range_lo(int64_t total, int i, int grid) {
+  return total * i / grid;
+}
+
+// record layout: [slot][G][4 + D]: m (log2 domain), l, -, -, acc[128] (HT
+// domain); slot = (unit + cta) * NGRP + group.
+template <int G>
+__device__ __forceinline__ float *record_ptr(float *recs, int slot) {
+  return recs + (int64_t)slot * G * (4 + D);
+}
+
+// channel of the K-side MMA k-index (thread t, k-tile kt, column group r,
+// element i): thread t owns the whole sub-vectors 4t..4t+3 of each token.
+__device__ __forceinline__ int k_channel(int t, int kt, int r, int i) {
+  return 32 * t + 8 * (kt >> 1) + 4 * (kt & 1) + 2 * r + i;
+}
+
+// ---------------------------------------------------------------------------
+// the fused kernel
+// ---------------------------------------------------------------------------
+template <int G, bool FOLD, bool HILO>
+__global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
+    attend_kernel(CacheViewDev cv, const float *__restrict__ qg, float *__restrict__ recs,
+                  int64_t total_chunks) {
+  constexpr int NT = AttCfg<G>::NT;
+  constexpr int NGRP = AttCfg<G>::NGRP;
+  constexpr int NSTAGE = AttCfg<G>::NSTAGE;
+  static_assert(sizeof(AttMisc<G>) <= MISC_MAX, "decode scratch does not fit below the tables");
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int n_units = cv.batch * cv.n_kv_heads;
+  const PageLayout L = page_layout(FOLD ? 2 : 1);
+  const uint32_t page_bytes = (uint32_t)L.bytes;
+
+  // ---- shared memory carve-up: tables at 64 KB-aligned shared addresses ----
+  const uint32_t base = smem_u32(smem);
+  const uint32_t tk = (base & 0xffffu) == 0 ? base : ((base + 0xffffu) & ~0xffffu);
+  const uint32_t tv = tk + 0x10000u;
+  // scratch below the tables (or above them when the window is 64 KB-aligned)
+  AttMisc<G> &M = *reinterpret_cast<AttMisc<G> *>(smem + ((base & 0xffffu) == 0 ? 0x20000u : 0u));
+
+  const int grid = gridDim.x;
+  const int64_t lo = range_lo(total_chunks, blockIdx.x, grid);
+  const int64_t hi = range_lo(total_chunks, blockIdx.x + 1, grid);
+  if (lo >= hi) return;
+
+  // stage loader: chunk k of the CTA range goes to stage k % NSTAGE
+  auto load_chunk = [&](int k, const ChunkCursor &c) {
+    const int s = k % NSTAGE;
+    const int64_t page = cv.page_table[(int64_t)c.u * cv.page_table_stride + c.c];
+    const int64_t p0 = cv.base_pos[c.u] + (int64_t)c.c * R - cv.rope_pos0;
+    uint8_t *st = M.st[s];
+    mbar_expect_tx(&M.full[s], 2 * page_bytes + ROPE_ROW_BYTES);
+    tma_load_1d(st, cv.k_pool + page * page_bytes, page_bytes, &M.full[s]);
+    tma_load_1d(st + page_bytes, cv.v_pool + page * page_bytes, page_bytes, &M.full[s]);
+    tma_load_1d(st + 2 * page_bytes, cv.rope_cs + p0 * NPAIR, ROPE_ROW_BYTES, &M.full[s]);
+  };
+  const int n_local = (int)(hi - lo);
+
+  if (warp == 0) {
+    ChunkCursor c0 = cursor_seek(lo, cv.n_chunks, n_units);
+    if (lane == 0) {
+      for (int s = 0; s < NSTAGE; ++s) mbar_init(&M.full[s], 1);
+      for (int q = 0; q < NGRP; ++q) {
+        mbar_init(&M.pro[q][0], 128);
+        mbar_init(&M.pro[q][1], 128);
+      }
+      mbar_init(&M.tabs, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      // codeword gather tables (2 x 64 KB) by bulk copy, overlapped with the
+      // first pages and the set-up
+      mbar_expect_tx(&M.tabs, 2 * 65536);
+      tma_load_1d(smem + (tk - base), cv.cb_k.tabw, 65536, &M.tabs);
+      tma_load_1d(smem + (tv - base), cv.cb_v.tabw, 65536, &M.tabs);
+      for (int k = 0; k < NSTAGE && k < n_local; ++k) {
+        load_chunk(k, c0);
+        cursor_advance(c0, cv.n_chunks, n_units);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ========================= consumer warps ==================================
+  const int grp = warp >> 2;   // consumer group: chunks i with i % NGRP == grp
+  const int ws = warp & 3;     // token slice [16 ws, 16 ws + 16)
+  const int ci = 32 * ws + lane;
+  const int bar_id = 1 + grp;
+  AttGroup<G> &S = M.grp[grp];
+  const bool leader = ws == 0 && lane == 0;
+
+  // constant o-term A fragments: (cos, sin)(tau f_j), tau = 16ws + g (+8),
+  // j = 8kt + t (+4), from table rows 0..63 (positions tau).
+  uint32_t tabA[8][4];
+#pragma unroll
+  for (int kt = 0; kt < 8; ++kt) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int tau = 16 * ws + g + ((r & 1) ? 8 : 0);
+      const int j = 8 * kt + t + ((r & 2) ? 4 : 0);
+      const float2 cs = cv.rope_cs[(int64_t)(tau - cv.rope_pos0) * NPAIR + j];
+      tabA[kt][r] = pack_h2(cs.x, cs.y);
+    }
+  }
+
+  // gather bases: PRMT drops the index byte into bits 8..15 of
+  // [table 64 KB base | idx << 8 | slot << 4]; slot = lane % 8 keeps every
+  // quarter-warp of 16-byte loads on 8 distinct bank groups.
+  const uint32_t slot16 = (uint32_t)((lane & 7) * 16);
+  const uint32_t lbk = (tk & 0xffff0000u) | slot16;
+  const uint32_t lbv = (tv & 0xffff0000u) | slot16;
+  const uint32_t vsel0 = 0x7604u | ((uint32_t)(2 * (g & 1)) << 4);
+  const uint32_t vsel1 = 0x7604u | ((uint32_t)(2 * (g & 1) + 1) << 4);
+  const uint32_t psel = (g & 1) ? 0x7632u : 0x5410u;  // P' part (hi/lo) selector
+
+  uint32_t qB[NT][8][2];
+  float accV[NT][8][4];
+  float m_run[NT], l_run[NT];
+
+  auto flush_unit = [&](int unit) {
+    named_bar(bar_id, 128);  // the merge buffers alias the per-chunk buffers
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float l = l_run[nt];
+      l += __shfl_xor_sync(0xffffffffu, l, 4);
+      l += __shfl_xor_sync(0xffffffffu, l, 8);
+      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      const int h = 4 * nt + t;
+      if (h < G) {
+        if (g == 0) {
+          S.mg.ml[ws][h][0] = m_run[nt];
+          S.mg.ml[ws][h][1] = l;
+        }
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          const int c = 16 * g + 8 * (mt >> 2) + 2 * (mt & 3);
+          S.mg.mrg[ws][h][c] = accV[nt][mt][0] + accV[nt][mt][1];
+          S.mg.mrg[ws][h][c + 1] = accV[nt][mt][2] + accV[nt][mt][3];
+        }
+      }
+    }
+    named_bar(bar_id, 128);
+    float *rec = record_ptr<G>(recs, (unit + blockIdx.x) * NGRP + grp);
+    for (int i = ci; i < G * D; i += 128) {
+      const int h = i / D, c = i - h * D;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int w2 = 0; w2 < 4; ++w2) mx = fmaxf(mx, S.mg.ml[w2][h][0]);
+      float a = 0.f, l = 0.f;
+      if (mx > -INFINITY) {
+#pragma unroll
+        for (int w2 = 0; w2 < 4; ++w2) {
+          const float sc = exp2f(S.mg.ml[w2][h][0] - mx);
+          a = fmaf(S.mg.mrg[w2][h][c], sc, a);
+          l = fmaf(S.mg.ml[w2][h][1], sc, l);
+        }
+      }
+      rec[h * (4 + D) + 4 + c] = a;
+      if (c == 0) {
+        rec[h * (4 + D) + 0] = mx;
+        rec[h * (4 + D) + 1] = l;
+      }
+    }
+    named_bar(bar_id, 128);
+  };
+
+  auto setup_unit = [&](int unit) {
+    const int b = unit / cv.n_kv_heads, hk = unit - b * cv.n_kv_heads;
+    const float *qs = qg + ((int64_t)b * cv.n_q_heads + (int64_t)hk * G) * D;
+    for (int i = ci; i < G * D; i += 128) S.q[i / D][i % D] = qs[i];
+    named_bar(bar_id, 128);
+    for (int h = ws; h < G; h += 4) {  // HT(q), 4 values per lane
+      float4 v = *reinterpret_cast<float4 *>(&S.q[h][4 * lane]);
+      float a = v.x + v.y, bq = v.x - v.y, c = v.z + v.w, d = v.z - v.w;
+      v.x = a + c; v.z = a - c; v.y = bq + d; v.w = bq - d;
+#pragma unroll
+      for (int m = 1; m < 32; m <<= 1) {
+        const float ox = __shfl_xor_sync(0xffffffffu, v.x, m);
+        const float oy = __shfl_xor_sync(0xffffffffu, v.y, m);
+        const float oz = __shfl_xor_sync(0xffffffffu, v.z, m);
+        const float ow = __shfl_xor_sync(0xffffffffu, v.w, m);
+        if (lane & m) {
+          v.x = ox - v.x; v.y = oy - v.y; v.z = oz - v.z; v.w = ow - v.w;
+        } else {
+          v.x += ox; v.y += oy; v.z += oz; v.w += ow;
+        }
+      }
+      const float sc = 0.08838834764831845f;
+      v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+      *reinterpret_cast<float4 *>(&S.ck.qh[h][4 * lane]) = v;
+    }
+    named_bar(bar_id, 128);
+    // B fragments of HT(q) in the permuted channel order; column n = g is
+    // (head 4nt + g/2, part g&1)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int h = 4 * nt + (g >> 1);
+#pragma unroll
+      for (int kt = 0; kt < 8; ++kt) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          float v0 = 0.f, v1 = 0.f;
+          if (h < G) {
+            float h0, l0, h1, l1;
+            split_h(S.ck.qh[h][k_channel(t, kt, r, 0)], h0, l0);
+            split_h(S.ck.qh[h][k_channel(t, kt, r, 1)], h1, l1);
+            v0 = (g & 1) ? l0 : h0;
+            v1 = (g & 1) ? l1 : h1;
+          }
+          qB[nt][kt][r] = pack_h2(v0, v1);
+        }
+      }
+      m_run[nt] = -INFINITY;
+      l_run[nt] = 0.f;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) accV[nt][mt][r] = 0.f;
+    }
+    named_bar(bar_id, 128);  // HT(q) aliases the per-chunk buffers
+  };
+
+  // the group walks its own chunks i = grp, grp + NGRP, ... of the range
+  ChunkCursor cur = cursor_seek(lo + grp, cv.n_chunks, n_units);
+  // the group leader refills the stage its previous chunk released: chunk
+  // i - NGRP + NSTAGE, issued once the prologue barrier of chunk i shows every
+  // warp of the group past chunk i - NGRP
+  ChunkCursor ahead = cursor_seek(lo + NSTAGE + grp, cv.n_chunks, n_units);
+  int cur_unit = -1;
+  bool tabs_ready = false;
+  int nloc = 0;  // chunks processed by this group (prologue slot parity)
+
+  for (int i = grp; i < n_local; i += NGRP) {
+    if (cur.u != cur_unit) {
+      if (cur_unit >= 0) flush_unit(cur_unit);
+      setup_unit(cur.u);
+      cur_unit = cur.u;
+    }
+    const int s = i % NSTAGE;
+    const int slot = nloc & 1;
+    const uint32_t pro_parity = (uint32_t)(nloc >> 1) & 1u;
+    ++nloc;
+    mbar_wait(&M.full[s], (uint32_t)(i / NSTAGE) & 1u);
+    if (!tabs_ready) {
+      mbar_wait(&M.tabs, 0);
+      tabs_ready = true;
+    }
+    const uint8_t *kp = M.st[s];
+    const uint8_t *vp = M.st[s] + page_bytes;
+    const float2 *rrow = reinterpret_cast<const float2 *>(M.st[s] + 2 * page_bytes);
+
+    // ---- cooperative chunk prologue (group of 4 warps) ----------------------
+    {
+      // (a) token scales: threads 0..63 keys, 64..127 values
+      const int tok = ci & 63;
+      const uint8_t *pg = ci < 64 ? kp : vp;
+      const uint16_t *par = reinterpret_cast<const uint16_t *>(pg + L.par);
+      const float s1sc = f16_bits_to_f32(par[0]), s1z = f16_bits_to_f32(par[1]);
+      const uint32_t nb = pg[L.s1n + (tok >> 1)];
+      const float lv = (float)((tok & 1) ? (nb >> 4) : (nb & 15u));
+      const float s1 = __fadd_rn(s1z, __fmul_rn(lv, s1sc));
+      const float s2 = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(pg + L.s2)[tok]);
+      float2 *scp = reinterpret_cast<float2 *>(&S.ck.sc[slot][tok]);
+      scp[ci < 64 ? 0 : 1] = make_float2(s1 * s2, s1);
+      // (b) value shift vector, one channel per thread
+      {
+        const uint16_t *pv = reinterpret_cast<const uint16_t *>(vp + L.par);
+        const int c = ci, gr = c >> 5;
+        const uint32_t b = vp[L.on + (c >> 1)];
+        const float l2 = (float)((c & 1) ? (b >> 4) : (b & 15u));
+        S.ck.ov[slot][c] = __fadd_rn(f16_bits_to_f32(pv[6 + gr]),
+                                  __fmul_rn(l2, f16_bits_to_f32(pv[2 + gr])));
+      }
+      // (c) o-term B fragments: warp ws owns pairs j in [16ws, 16ws + 16)
+      {
+        const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + L.par);
+        const int j = 16 * ws + (lane >> 1);
+        const int gr = (2 * j) >> 5;
+        const uint32_t b = kp[L.on + j];
+        const float osc = f16_bits_to_f32(pk[2 + gr]), oz = f16_bits_to_f32(pk[6 + gr]);
+        const float oe = __fadd_rn(oz, __fmul_rn((float)(b & 15u), osc));
+        const float oo = __fadd_rn(oz, __fmul_rn((float)(b >> 4), osc));
+        const float2 cs = rrow[j];
+        const float he = oe * cs.x - oo * cs.y;  // RoPE(o, p0)
+        const float ho = oe * cs.y + oo * cs.x;
+        const int kt = j >> 3, tt = j & 3, half = (j >> 2) & 1;
+#pragma unroll
+        for (int h = (lane & 1); h < 4 * NT; h += 2) {
+          float al = 0.f, be = 0.f;
+          if (h < G) {
+            const float qe = S.q[h][2 * j], qo = S.q[h][2 * j + 1];
+            al = qe * he + qo * ho;
+            be = qo * he - qe * ho;
+          }
+          float ah, alo, bh, blo;
+          split_h(al, ah, alo);
+          split_h(be, bh, blo);
+          const int nt = h >> 2, hh = h & 3;
+          reinterpret_cast<uint32_t *>(&S.ck.ab[slot][nt][kt][4 * (2 * hh) + tt])[half] = pack_h2(ah, bh);
+          reinterpret_cast<uint32_t *>(&S.ck.ab[slot][nt][kt][4 * (2 * hh + 1) + tt])[half] = pack_h2(alo, blo);
+        }
+      }
+    }
+    mbar_arrive(&M.pro[grp][slot]);
+    if (i >= NGRP) {
+      if (leader) {  // every warp of the group is past chunk i - NGRP
+        mbar_wait(&M.pro[grp][slot], pro_parity);
+        if (i - NGRP + NSTAGE < n_local) load_chunk(i - NGRP + NSTAGE, ahead);
+      }
+#pragma unroll
+      for (int a2 = 0; a2 < NGRP; ++a2) cursor_advance(ahead, cv.n_chunks, n_units);
+    }
+
+    // ---- K side: payload dot products on tensor cores ------------------------
+    const int tok0 = 16 * ws + g, tok1 = tok0 + 8;
+    const uint32_t kpa = smem_u32(kp);
+    const uint32_t ik0 = lds32(kpa + L.idx + tok0 * NSUB + 4 * t);
+    const uint32_t ik1 = lds32(kpa + L.idx + tok1 * NSUB + 4 * t);
+    uint32_t sk0 = 0, sk1 = 0;
+    if (FOLD) {
+      sk0 = lds32(kpa + L.sgn + tok0 * 16 + 4 * t);
+      sk1 = lds32(kpa + L.sgn + tok1 * 16 + 4 * t);
+    }
+    float d1[NT][2][4], d2[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) d1[nt][0][r] = d1[nt][1][r] = d2[nt][r] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {  // item m = sub 4t + m of tokens g, g+8
+      const uint32_t sel = 0x7604u | ((uint32_t)m << 4);
+      const uint32_t a0 = prmt(ik0, lbk, sel), a1 = prmt(ik1, lbk, sel);
+      uint4 h0 = lds128(a0), h1 = lds128(a1);
+      uint4 l0 = make_uint4(0, 0, 0, 0), l1 = l0;
+      if (HILO) {
+        l0 = lds128(a0 + 128);
+        l1 = lds128(a1 + 128);
+      }
+      if (FOLD) {
+        uint32_t *ph0 = &h0.x, *ph1 = &h1.x, *pl0 = &l0.x, *pl1 = &l1.x;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t w0 = sk0 << (15 - 4 * m - p);
+          const uint32_t w1 = sk1 << (15 - 4 * m - p);
+          ph0[p] = xor_sign(ph0[p], w0);
+          ph1[p] = xor_sign(ph1[p], w1);
+          if (HILO) {
+            pl0[p] = xor_sign(pl0[p], w0);
+            pl1[p] = xor_sign(pl1[p], w1);
+          }
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        // k-tile 2m: pairs 0 (cols 2t..) and 1 (cols 2t+8..); k-tile 2m+1: pairs 2, 3
+        mma16816(d1[nt][0], h0.x, h1.x, h0.y, h1.y, qB[nt][2 * m][0], qB[nt][2 * m][1]);
+        mma16816(d1[nt][1], h0.z, h1.z, h0.w, h1.w, qB[nt][2 * m + 1][0], qB[nt][2 * m + 1][1]);
+        if (HILO) {
+          mma16816(d1[nt][0], l0.x, l1.x, l0.y, l1.y, qB[nt][2 * m][0], qB[nt][2 * m][1]);
+          mma16816(d1[nt][1], l0.z, l1.z, l0.w, l1.w, qB[nt][2 * m + 1][0], qB[nt][2 * m + 1][1]);
+        }
+      }
+    }
+    mbar_wait(&M.pro[grp][slot], pro_parity);  // AB, scales, o_v of the group
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int kt = 0; kt < 8; ++kt) {
+        const uint2 ab = *reinterpret_cast<const uint2 *>(&S.ck.ab[slot][nt][kt][lane]);
+        mma16816(d2[nt], tabA[kt][0], tabA[kt][1], tabA[kt][2], tabA[kt][3], ab.x, ab.y);
+      }
+    }
+
+    // ---- scores and online softmax (base 2) ---------------------------------
+    const float4 sc0 = S.ck.sc[slot][tok0];
+    const float4 sc1 = S.ck.sc[slot][tok1];
+    uint32_t pf[NT][2];
+    float wsum[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int h = 4 * nt + t;
+      const float pd0 = (d1[nt][0][0] + d1[nt][1][0]) + (d1[nt][0][1] + d1[nt][1][1]);
+      const float pd1 = (d1[nt][0][2] + d1[nt][1][2]) + (d1[nt][0][3] + d1[nt][1][3]);
+      const float x0 = (sc0.x * pd0 + sc0.y * (d2[nt][0] + d2[nt][1])) * LOG2E_OVER_SQRTD;
+      const float x1 = (sc1.x * pd1 + sc1.y * (d2[nt][2] + d2[nt][3])) * LOG2E_OVER_SQRTD;
+      float mx = fmaxf(x0, x1);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      const float m_new = fmaxf(m_run[nt], mx);
+      if (m_new > m_run[nt]) {
+        const float r = exp2f(m_run[nt] - m_new);
+        l_run[nt] *= r;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) accV[nt][mt][q] *= r;
+        m_run[nt] = m_new;
+      }
+      float p0 = exp2f(x0 - m_new), p1 = exp2f(x1 - m_new);
+      if (h >= G) p0 = p1 = 0.f;
+      l_run[nt] += p0 + p1;
+      // value weights: P' = p * s1v * s2v (codewords), W = sum p * s1v (shift)
+      float ws2 = p0 * sc0.w + p1 * sc1.w;
+      ws2 += __shfl_xor_sync(0xffffffffu, ws2, 4);
+      ws2 += __shfl_xor_sync(0xffffffffu, ws2, 8);
+      ws2 += __shfl_xor_sync(0xffffffffu, ws2, 16);
+      wsum[nt] = ws2;
+      float h0, l0, h1, l1;
+      split_h(p0 * sc0.z, h0, l0);
+      split_h(p1 * sc1.z, h1, l1);
+      const uint32_t X0 = pack_h2(h0, l0);  // token g   (hi, lo)
+      const uint32_t X1 = pack_h2(h1, l1);  // token g+8
+      // B fragment of P': column g = (head 4nt + g/2, part g&1); rows are the
+      // tokens 2t, 2t+1 (reg 0) and 2t+8, 2t+9 (reg 1) of the warp's slice
+      const int hs = g >> 1;
+      const int srcA = 8 * t + hs, srcB = 8 * t + 4 + hs;
+      const uint32_t y0a = __shfl_sync(0xffffffffu, X0, srcA);
+      const uint32_t y0b = __shfl_sync(0xffffffffu, X0, srcB);
+      const uint32_t y1a = __shfl_sync(0xffffffffu, X1, srcA);
+      const uint32_t y1b = __shfl_sync(0xffffffffu, X1, srcB);
+      pf[nt][0] = prmt(y0a, y0b, psel);
+      pf[nt][1] = prmt(y1a, y1b, psel);
+    }
+
+    // ---- V side: accumulate P' . codewords on tensor cores -------------------
+    // thread (g, t): tokens 2t, 2t+1, 2t+8, 2t+9 of the slice; subs 2g, 2g+1
+    const uint32_t vpa = smem_u32(vp);
+    const int vt0 = 16 * ws + 2 * t;
+    uint32_t iv[4], sv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tok = vt0 + (q & 1) + ((q & 2) ? 8 : 0);
+      iv[q] = lds32(vpa + L.idx + tok * NSUB + 4 * (g >> 1));
+      sv[q] = FOLD ? (lds32(vpa + L.sgn + tok * 16 + 4 * (g >> 1)) >> (8 * (g & 1))) : 0u;
+    }
+#pragma unroll
+    for (int sg = 0; sg < 2; ++sg) {  // sub 2g + sg
+      const uint32_t sel = sg ? vsel1 : vsel0;
+      uint4 yh[4], yl[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t a = prmt(iv[q], lbv, sel);
+        yh[q] = lds128(a);
+        yl[q] = HILO ? lds128(a + 128) : make_uint4(0, 0, 0, 0);
+        if (FOLD) {
+          uint32_t *ph = &yh[q].x, *pl = &yl[q].x;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const uint32_t wk = sv[q] << (15 - 4 * sg - p);
+            ph[p] = xor_sign(ph[p], wk);
+            if (HILO) pl[p] = xor_sign(pl[p], wk);
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {  // m-tile 4 sg + p: channels 16g + 8sg + 2p (+1)
+        const int mt = 4 * sg + p;
+        const uint32_t *h0p = &yh[0].x, *h1p = &yh[1].x, *h2p = &yh[2].x, *h3p = &yh[3].x;
+        const uint32_t a0h = prmt(h0p[p], h1p[p], 0x5410u), a1h = prmt(h0p[p], h1p[p], 0x7632u);
+        const uint32_t a2h = prmt(h2p[p], h3p[p], 0x5410u), a3h = prmt(h2p[p], h3p[p], 0x7632u);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          mma16816(accV[nt][mt], a0h, a1h, a2h, a3h, pf[nt][0], pf[nt][1]);
+        if (HILO) {
+          const uint32_t *l0p = &yl[0].x, *l1p = &yl[1].x, *l2p = &yl[2].x, *l3p = &yl[3].x;
+          const uint32_t a0l = prmt(l0p[p], l1p[p], 0x5410u), a1l = prmt(l0p[p], l1p[p], 0x7632u);
+          const uint32_t a2l = prmt(l2p[p], l3p[p], 0x5410u), a3l = prmt(l2p[p], l3p[p], 0x7632u);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            mma16816(accV[nt][mt], a0l, a1l, a2l, a3l, pf[nt][0], pf[nt][1]);
+        }
+      }
+    }
+    // value shift vector: acc[c] += W * o_v[c] for the thread's 16 channels
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const float4 o4 = *reinterpret_cast<const float4 *>(&S.ck.ov[slot][16 * g + 4 * q4]);
+      // channels 16g + 4q4 + {0,1,2,3}: m-tiles (sg = q4 >> 1, p = 2 (q4 & 1) + {0, 1})
+      const int mt0 = 4 * (q4 >> 1) + 2 * (q4 & 1);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        accV[nt][mt0][0] = fmaf(wsum[nt], o4.x, accV[nt][mt0][0]);
+        accV[nt][mt0][2] = fmaf(wsum[nt], o4.y, accV[nt][mt0][2]);
+        accV[nt][mt0 + 1][0] = fmaf(wsum[nt], o4.z, accV[nt][mt0 + 1][0]);
+        accV[nt][mt0 + 1][2] = fmaf(wsum[nt], o4.w, accV[nt][mt0 + 1][2]);
+      }
+    }
+#pragma unroll
+    for (int a2 = 0; a2 < NGRP; ++a2) cursor_advance(cur, cv.n_chunks, n_units);
+  }
+  if (cur_unit >= 0) flush_unit(cur_unit);
+}
+
+// ---------------------------------------------------------------------------
+// combine: merge the stream-K records of a unit with its exact residual rows,
+// normalise, inverse FWHT (attention.py:105-108, 129-133, 141).
+// One CTA (128 threads) per (batch, q-head).
+// ---------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(128) combine_kernel(CacheViewDev cv, const float *__restrict__ qg,
+                                                      const float *__restrict__ recs,
+                                                      int64_t total_chunks, int grid,
+                                                      float *__restrict__ out,
                                                       float *__restrict__ lse) {
-  __shared__ double red[256];
+  __shared__ float s_acc[D];
+  __shared__ float s_w[R];
+  __shared__ float s_q[D];
+  __shared__ int64_t s_red[128];
   const int row = blockIdx.x;
   const int b = row / cv.n_q_heads, i = row - b * cv.n_q_heads;
-  const int G = cv.n_q_heads / cv.n_kv_heads;
-  const int u = b * cv.n_kv_heads + i / G;
-  const int n = cv.n_chunks[u] * R + cv.n_res[u];
-  float *s = sw + (int64_t)row * cv.max_tokens;
-  const double inv_sqrt_d = 1.0 / sqrt(128.0);
-  double mx = -1e300;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) mx = fmax(mx, (double)s[t] / sqrt(128.0));
-  red[threadIdx.x] = mx;
+  const int hk = i / G, h = i - hk * G;
+  const int u = b * cv.n_kv_heads + hk;
+  const int ch = threadIdx.x;
+  {
+    int64_t acc = 0;
+    for (int uu = ch; uu < u; uu += 128) acc += cv.n_chunks[uu];
+    s_red[ch] = acc;
+  }
+  s_q[ch] = qg[(int64_t)row * D + ch];
   __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (threadIdx.x < off) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + off]);
+  for (int off = 64; off > 0; off >>= 1) {
+    if (ch < off) s_red[ch] += s_red[ch + off];
     __syncthreads();
   }
-  mx = red[0];
-  __syncthreads();
-  double sum = 0.0;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) sum += exp((double)s[t] / sqrt(128.0) - mx);
-  red[threadIdx.x] = sum;
-  __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
-    __syncthreads();
+  const int64_t s_off = s_red[0];
+  const int nch = cv.n_chunks[u];
+  float m = -INFINITY, l = 0.f, a = 0.f;
+  if (nch > 0) {
+    const int64_t x0 = s_off, x1 = s_off + nch - 1;
+    int c0 = (int)(x0 * grid / total_chunks);
+    while (c0 + 1 < grid && range_lo(total_chunks, c0 + 1, grid) <= x0) ++c0;
+    while (c0 > 0 && range_lo(total_chunks, c0, grid) > x0) --c0;
+    int c1 = (int)(x1 * grid / total_chunks);
+    while (c1 + 1 < grid && range_lo(total_chunks, c1 + 1, grid) <= x1) ++c1;
+    while (c1 > 0 && range_lo(total_chunks, c1, grid) > x1) --c1;
+    constexpr int NGRP = AttCfg<G>::NGRP;
+    for (int c = c0; c <= c1; ++c) {
+      // local chunk indices of unit u inside CTA c; group gq owns k % NGRP == gq
+      const int64_t clo = range_lo(total_chunks, c, grid);
+      const int64_t chi = range_lo(total_chunks, c + 1, grid);
+      const int64_t ka = (x0 > clo ? x0 : clo) - clo;
+      const int64_t kb = (x1 + 1 < chi ? x1 + 1 : chi) - clo;
+      for (int gq = 0; gq < NGRP; ++gq) {
+        if (!(ka + ((gq - ka % NGRP + NGRP) % NGRP) < kb)) continue;
+        const float *rec = record_ptr<G>(const_cast<float *>(recs), (u + c) * NGRP + gq) + h * (4 + D);
+        const float rm = rec[0], rl = rec[1];
+        if (!(rm > -INFINITY)) continue;  // the group saw no chunk of this unit
+        const float mn = fmaxf(m, rm);
+        const float sa = exp2f(m - mn), sb = exp2f(rm - mn);
+        a = a * sa + rec[4 + ch] * sb;
+        l = l * sa + rl * sb;
+        m = mn;
+      }
+    }
   }
-  sum = red[0];
-  for (int t = threadIdx.x; t < n; t += blockDim.x)
-    s[t] = (float)(exp((double)s[t] / sqrt(128.0) - mx) / sum);
-  if (lse && threadIdx.x == 0) lse[row] = (float)(mx + log(sum));
-  (void)inv_sqrt_d;
+  // residual rows: exact RoPE(k, pos) . q scores (base-2 logits)
+  const int nres = cv.n_res[u];
+  if (nres > 0) {
+    const int64_t pbase = cv.base_pos[u] + (int64_t)nch * R;
+    if (ch < nres) {
+      const float *kr = cv.k_res + ((int64_t)u * R + ch) * D;
+      const float2 *cs = cv.rope_cs + (pbase + ch - cv.rope_pos0) * NPAIR;
+      float acc = 0.f;
+      for (int j = 0; j < NPAIR; ++j) {
+        const float2 e = cs[j];
+        const float ke = kr[2 * j], ko = kr[2 * j + 1];
+        acc = fmaf(ke * e.x - ko * e.y, s_q[2 * j], acc);
+        acc = fmaf(ke * e.y + ko * e.x, s_q[2 * j + 1], acc);
+      }
+      s_w[ch] = acc * LOG2E_OVER_SQRTD;
+    }
+    __syncthreads();
+    float rm = -INFINITY;
+    for (int tt = 0; tt < nres; ++tt) rm = fmaxf(rm, s_w[tt]);
+    const float mn = fmaxf(m, rm);
+    const float sa = (m > -INFINITY) ? exp2f(m - mn) : 0.f;
+    a *= sa;
+    l *= sa;
+    for (int tt = 0; tt < nres; ++tt) {
+      const float p = exp2f(s_w[tt] - mn);
+      l += p;
+      a = fmaf(p, cv.v_res[((int64_t)u * R + tt) * D + ch], a);
+    }
+    m = mn;
+  }
+  s_acc[ch] = (l > 0.f) ? a / l : 0.f;
+  __syncthreads();
+  block_fwht128(s_acc);
+  out[(int64_t)row * D + ch] = s_acc[ch];
+  if (lse && ch == 0) lse[row] = (l > 0.f) ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
 }
 
 }  // namespace nsnkv
 
 using namespace nsnkv;
 
-static size_t scores_bytes(const CacheViewDev &cv) {
-  return ((size_t)cv.batch * cv.n_q_heads * cv.max_tokens * sizeof(float) + 255) / 256 * 256;
+static int attend_grid() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+static size_t records_bytes(const CacheViewDev &cv, int G) {
+  const int units = cv.batch * cv.n_kv_heads;
+  return (size_t)(units + attend_grid() + 1) * 2 * G * (4 + D) * sizeof(float);
 }
 
 extern "C" size_t nsnkv_decode_workspace_bytes(const nsnkv_cache_view *cv_in) {
   CacheViewDev cv;
   if (make_cache_view(cv_in, &cv)) return 0;
-  return scores_bytes(cv) + nsnkv_internal_output_ws(cv);
+  const int G = cv.n_q_heads / cv.n_kv_heads;
+  const size_t a = (records_bytes(cv, G) + 255) / 256 * 256;
+  const size_t b = nsnkv_internal_output_ws(cv);
+  return a > b ? a : b;
+}
+
+template <int G, bool FOLD, bool HILO>
+static int launch_attend(const CacheViewDev &cv, const float *q, float *out, float *lse,
+                         float *recs, int64_t total, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attend_kernel<G, FOLD, HILO>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM_BYTES);
+    attr = true;
+  }
+  int grid = attend_grid();
+  if (total < grid) grid = (int)(total > 0 ? total : 1);
+  int launches = 1;
+  if (total > 0) {
+    attend_kernel<G, FOLD, HILO>
+        <<<grid, AttCfg<G>::THREADS, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
+    ++launches;
+  }
+  combine_kernel<G><<<cv.batch * cv.n_q_heads, 128, 0, st>>>(cv, q, recs, total > 0 ? total : 1,
+                                                              grid, out, lse);
+  nsnkv_internal_count_launch(launches);
+  return nsnkv_internal_check_launch("decode_attend");
 }
 
 extern "C" int nsnkv_decode_attend(const nsnkv_cache_view *cv_in, const float *q, float *out,
@@ -63,15 +858,39 @@ extern "C" int nsnkv_decode_attend(const nsnkv_cache_view *cv_in, const float *q
   CacheViewDev cv;
   int rc = make_cache_view(cv_in, &cv);
   if (rc) return rc;
-  const size_t sb = scores_bytes(cv);
-  if (workspace_bytes < sb + nsnkv_internal_output_ws(cv))
+  const int G = cv.n_q_heads / cv.n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8)
+    return nsnkv_internal_set_error(NSNKV_ERR_UNSUPPORTED, "decode_attend: GQA group must be 1, 2, 4 or 8");
+  if (cv.rope_pos0 != 0)
+    return nsnkv_internal_set_error(NSNKV_ERR_UNSUPPORTED, "decode_attend: RoPE table must start at position 0");
+  if (workspace_bytes < records_bytes(cv, G))
     return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "decode_attend: workspace too small");
-  float *sw = (float *)workspace;
-  rc = nsnkv_decode_scores(cv_in, q, sw, stream);
-  if (rc) return rc;
-  softmax_kernel<<<cv.batch * cv.n_q_heads, 256, 0, (cudaStream_t)stream>>>(cv, sw, lse);
-  nsnkv_internal_count_launch(1);
-  rc = nsnkv_internal_check_launch("decode_softmax");
-  if (rc) return rc;
-  return nsnkv_decode_output(cv_in, sw, out, (char *)workspace + sb, workspace_bytes - sb, stream);
+  const int units = cv.batch * cv.n_kv_heads;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t total = cv.total_chunks;
+  if (total < 0) {  // read the counts back (synchronises the stream)
+    int32_t *h = (int32_t *)malloc(sizeof(int32_t) * units);
+    cudaError_t e = cudaMemcpyAsync(h, cv.n_chunks, sizeof(int32_t) * units,
+                                    cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    total = 0;
+    for (int u = 0; !e && u < units; ++u) total += h[u];
+    free(h);
+    if (e) return nsnkv_internal_set_error(NSNKV_ERR_CUDA, cudaGetErrorString(e));
+  }
+  float *recs = (float *)workspace;
+  const bool fold = cv.cb_k.bit_mode == 2;
+  const bool hilo = cv.fast_fp16 == 0;
+#define NSNKV_ATT(GG)                                                                    \
+  return fold ? (hilo ? launch_attend<GG, true, true>(cv, q, out, lse, recs, total, st)  \
+                      : launch_attend<GG, true, false>(cv, q, out, lse, recs, total, st)) \
+              : (hilo ? launch_attend<GG, false, true>(cv, q, out, lse, recs, total, st) \
+                      : launch_attend<GG, false, false>(cv, q, out, lse, recs, total, st))
+  switch (G) {
+    case 1: NSNKV_ATT(1);
+    case 2: NSNKV_ATT(2);
+    case 4: NSNKV_ATT(4);
+    default: NSNKV_ATT(8);
+  }
+#undef NSNKV_ATT
 }

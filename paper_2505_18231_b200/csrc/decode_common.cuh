@@ -17,6 +17,8 @@ struct CacheViewDev {
   const float2 *rope_cs;
   int64_t rope_pos0, rope_n;
   CodebookDev cb_k, cb_v;
+  int64_t total_chunks;
+  int fast_fp16;
 };
 
 struct ChunkMeta {
@@ -56,12 +58,13 @@ __device__ __forceinline__ float dequant_o(const uint8_t *page, const PageLayout
 // Natural sign byte of (token t, sub j) from the bit-permuted page words.
 __device__ __forceinline__ uint32_t sign_byte(const uint8_t *page, const PageLayout &L, int t,
                                               int j) {
-  const uint32_t *w = reinterpret_cast<const uint32_t *>(page + L.sgn) + 4 * t;
+  const uint32_t w = reinterpret_cast<const uint32_t *>(page + L.sgn)[4 * t + (j >> 2)];
+  const int m = j & 3;
   uint32_t b = 0;
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    b |= ((w[p] >> j) & 1u) << (2 * p);
-    b |= ((w[p] >> (16 + j)) & 1u) << (2 * p + 1);
+    b |= ((w >> (4 * m + p)) & 1u) << (2 * p);
+    b |= ((w >> (16 + 4 * m + p)) & 1u) << (2 * p + 1);
   }
   return b;
 }

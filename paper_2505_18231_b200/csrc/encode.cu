@@ -292,14 +292,17 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_chunks_kernel(
     const uint32_t w = *reinterpret_cast<const uint32_t *>(&s.idx[0][0] + 4 * tid);
     *reinterpret_cast<uint32_t *>(page + L.idx + 4 * tid) = w;
   }
-  if (fold) {  // bit-permuted signs: word p of token t
-    const int t = tid >> 2, p = tid & 3;
+  if (fold) {  // bit-permuted signs: word q of token t covers subs 4q..4q+3
+    const int t = tid >> 2, q = tid & 3;
     uint32_t w = 0;
 #pragma unroll
-    for (int j = 0; j < NSUB; ++j) {
-      const uint32_t b = s.sgn[t][j];
-      w |= ((b >> (2 * p)) & 1u) << j;
-      w |= ((b >> (2 * p + 1)) & 1u) << (16 + j);
+    for (int m = 0; m < 4; ++m) {
+      const uint32_t b = s.sgn[t][4 * q + m];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        w |= ((b >> (2 * p)) & 1u) << (4 * m + p);
+        w |= ((b >> (2 * p + 1)) & 1u) << (16 + 4 * m + p);
+      }
     }
     *reinterpret_cast<uint32_t *>(page + L.sgn + 4 * tid) = w;
   }
