@@ -122,7 +122,7 @@ def test_decode_matches_reference(case):
         ref_s = g["scores"][i]
         assert np.max(np.abs(s - ref_s)) <= 1e-5 * max(1.0, np.max(np.abs(ref_s)))
         w, out = P.attend_quantized(q, st, cb, cb)
-        assert np.max(np.abs(w - g["weights"][i])) <= 1e-5
+        assert np.max(np.abs(w - g["weights"][i])) <= 1e-4 * g["weights"][i].max()
         ref_o = g["out"][i]
         assert np.max(np.abs(out - ref_o)) <= OUT_TOL * np.max(np.abs(ref_o))
         o2 = P.output_quantized(g["weights"][i], st, cb)
