@@ -172,12 +172,16 @@ def run_ours(args) -> dict | None:
     gen.manual_seed(99 + rank)
     q = torch.randn(B, Hq, D, device=device, generator=gen)
     out = torch.empty(B, Hq, D, device=device)
-    gathered = (torch.empty(world * B, Hq, D, device=device) if world > 1 else None)
+    # weak scaling: global batch B * world, each rank owns a contiguous batch
+    # range (paper_2505_18231_b200.sharding); one all-gather of outputs/step
+    from paper_2505_18231_b200.sharding import gather_outputs, plan_shards
+
+    plan = plan_shards(B * world, Hkv, Hq, world, rank)
 
     def step():
         cache.attend(q, out=out)
-        if gathered is not None:
-            torch.distributed.all_gather_into_tensor(gathered, out)
+        if world > 1:
+            gather_outputs(plan, out)
 
     def barrier():
         if world > 1:
