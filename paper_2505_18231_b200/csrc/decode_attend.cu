@@ -121,16 +121,17 @@ __device__ __forceinline__ void split_h(float x, float &hi, float &lo) {
 // ---------------------------------------------------------------------------
 constexpr int ROPE_ROW_BYTES = NPAIR * 8;        // 64 x (cos, sin) fp32
 constexpr int STAGE_BYTES = 2 * NSNKV_PAGE_BYTES_2B + ROPE_ROW_BYTES;
-constexpr int ATT_SMEM_BYTES = 196608;           // two 64 KB-aligned tables + misc
-constexpr int MISC_MAX = 65536 - 1024;           // below the tables (1 KB is reserved)
+constexpr int ATT_SMEM_BYTES = 232448;           // 227 KB: two 64 KB-aligned tables + misc
+constexpr int MISC_LO_MAX = 65536 - 1024;        // below the tables (1 KB is reserved)
+constexpr int MISC_HI_MAX = 232448 + 1024 - 196608;  // above the tables
 constexpr float LOG2E_OVER_SQRTD = 1.4426950408889634f * 0.08838834764831845f;
 
 template <int G>
 struct AttCfg {
   static constexpr int NT = (2 * G + 7) / 8;  // n-tiles of 8 (head, hi/lo) columns
-  static constexpr int NGRP = 2;               // consumer groups of 4 warps
+  static constexpr int NGRP = G <= 4 ? 3 : 1;  // consumer groups of 4 warps
   static constexpr int THREADS = 4 * NGRP * 32;
-  static constexpr int NSTAGE = G <= 4 ? 8 : 4; // page ring depth
+  static constexpr int NSTAGE = NGRP == 3 ? 9 : 8;  // page ring depth
 };
 
 // Per-group prologue / merge scratch.  The unit-merge buffers alias the
@@ -155,16 +156,20 @@ struct AttGroup {
   float q[G][D];              // RoPE'd q of the group's current unit
 };
 
-// Everything but the tables: stage ring, barriers and the two groups'
-// scratch (below the 64 KB-aligned tables).
+// Stage ring, constant shift-term fragments and barriers (below the 64
+// KB-aligned tables); the groups' scratch lives above the tables.
 template <int G>
 struct AttMisc {
   static constexpr int NSTAGE = AttCfg<G>::NSTAGE;
   __align__(128) uint8_t st[NSTAGE][STAGE_BYTES];
-  AttGroup<G> grp[AttCfg<G>::NGRP];
+  uint4 taba[4][8][32];               // (cos, sin)(tau f_j) A fragments per token slice
   uint64_t full[NSTAGE];
   uint64_t pro[AttCfg<G>::NGRP][2];   // per-group prologue barriers (2 slots)
   uint64_t tabs;
+};
+template <int G>
+struct AttGroups {
+  AttGroup<G> grp[AttCfg<G>::NGRP];
 };
 
 struct ChunkCursor {
@@ -234,7 +239,8 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
   constexpr int NT = AttCfg<G>::NT;
   constexpr int NGRP = AttCfg<G>::NGRP;
   constexpr int NSTAGE = AttCfg<G>::NSTAGE;
-  static_assert(sizeof(AttMisc<G>) <= MISC_MAX, "decode scratch does not fit below the tables");
+  static_assert(sizeof(AttMisc<G>) <= MISC_LO_MAX, "decode ring does not fit below the tables");
+  static_assert(sizeof(AttGroups<G>) <= MISC_HI_MAX, "decode scratch does not fit above the tables");
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -246,8 +252,13 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
   const uint32_t base = smem_u32(smem);
   const uint32_t tk = (base & 0xffffu) == 0 ? base : ((base + 0xffffu) & ~0xffffu);
   const uint32_t tv = tk + 0x10000u;
-  // scratch below the tables (or above them when the window is 64 KB-aligned)
-  AttMisc<G> &M = *reinterpret_cast<AttMisc<G> *>(smem + ((base & 0xffffu) == 0 ? 0x20000u : 0u));
+  // ring below the tables and scratch above them (both above the tables when
+  // the window happens to start 64 KB-aligned)
+  const bool aligned_window = (base & 0xffffu) == 0;
+  AttMisc<G> &M = *reinterpret_cast<AttMisc<G> *>(smem + (aligned_window ? 0x20000u : 0u));
+  AttGroups<G> &GS = *reinterpret_cast<AttGroups<G> *>(
+      smem + (tv + 0x10000u - base) +
+      (aligned_window ? (uint32_t)((sizeof(AttMisc<G>) + 127) / 128 * 128) : 0u));
 
   const int grid = gridDim.x;
   const int64_t lo = range_lo(total_chunks, blockIdx.x, grid);
@@ -295,22 +306,27 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
   const int ws = warp & 3;     // token slice [16 ws, 16 ws + 16)
   const int ci = 32 * ws + lane;
   const int bar_id = 1 + grp;
-  AttGroup<G> &S = M.grp[grp];
+  AttGroup<G> &S = GS.grp[grp];
   const bool leader = ws == 0 && lane == 0;
 
   // constant o-term A fragments: (cos, sin)(tau f_j), tau = 16ws + g (+8),
-  // j = 8kt + t (+4), from table rows 0..63 (positions tau).
-  uint32_t tabA[8][4];
+  // j = 8kt + t (+4), from table rows 0..63 (positions tau); built once by
+  // group 0 into shared memory (shared by all groups)
+  if (grp == 0) {
 #pragma unroll
-  for (int kt = 0; kt < 8; ++kt) {
+    for (int kt = 0; kt < 8; ++kt) {
+      uint32_t f[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int tau = 16 * ws + g + ((r & 1) ? 8 : 0);
-      const int j = 8 * kt + t + ((r & 2) ? 4 : 0);
-      const float2 cs = cv.rope_cs[(int64_t)(tau - cv.rope_pos0) * NPAIR + j];
-      tabA[kt][r] = pack_h2(cs.x, cs.y);
+      for (int r = 0; r < 4; ++r) {
+        const int tau = 16 * ws + g + ((r & 1) ? 8 : 0);
+        const int j = 8 * kt + t + ((r & 2) ? 4 : 0);
+        const float2 cs = cv.rope_cs[(int64_t)(tau - cv.rope_pos0) * NPAIR + j];
+        f[r] = pack_h2(cs.x, cs.y);
+      }
+      M.taba[ws][kt][lane] = make_uint4(f[0], f[1], f[2], f[3]);
     }
   }
+  __syncthreads();
 
   // gather bases: PRMT drops the index byte into bits 8..15 of
   // [table 64 KB base | idx << 8 | slot << 4]; slot = lane % 8 keeps every
@@ -576,7 +592,8 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
 #pragma unroll
       for (int kt = 0; kt < 8; ++kt) {
         const uint2 ab = *reinterpret_cast<const uint2 *>(&S.ck.ab[slot][nt][kt][lane]);
-        mma16816(d2[nt], tabA[kt][0], tabA[kt][1], tabA[kt][2], tabA[kt][3], ab.x, ab.y);
+        const uint4 ta = M.taba[ws][kt][lane];
+        mma16816(d2[nt], ta.x, ta.y, ta.z, ta.w, ab.x, ab.y);
       }
     }
 
@@ -817,7 +834,8 @@ static int attend_grid() {
 
 static size_t records_bytes(const CacheViewDev &cv, int G) {
   const int units = cv.batch * cv.n_kv_heads;
-  return (size_t)(units + attend_grid() + 1) * 2 * G * (4 + D) * sizeof(float);
+  const int ngrp = G <= 4 ? AttCfg<4>::NGRP : AttCfg<8>::NGRP;
+  return (size_t)(units + attend_grid() + 1) * ngrp * G * (4 + D) * sizeof(float);
 }
 
 extern "C" size_t nsnkv_decode_workspace_bytes(const nsnkv_cache_view *cv_in) {
