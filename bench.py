@@ -133,7 +133,7 @@ def dist_setup():
     return world, rank, local
 
 
-def build_cache(cfg_name: str, device, seed: int, fast_fp16: bool = False):
+def build_cache(cfg_name: str, device, seed: int, precision: str = "precise"):
     """Encode a synthetic cache of the workload shape with the product's own
     append path (chunked so fp32 staging stays small)."""
     import torch
@@ -144,7 +144,7 @@ def build_cache(cfg_name: str, device, seed: int, fast_fp16: bool = False):
     cb = P.default_codebook(f"{bm}b")
     cfg = P.CacheConfig(d=D, bit_mode=cb.bit_mode)
     cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, device=device,
-                           check_finite=False, fast_fp16=fast_fp16)
+                           check_finite=False, precision=precision)
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
     block = 4096
@@ -167,7 +167,7 @@ def run_ours(args) -> dict | None:
     world, rank, local = dist_setup()
     device = torch.device("cuda", local)
     B, Hq, Hkv, T, bm = CONFIGS[args.config]
-    cache = build_cache(args.config, device, seed=1234 + rank, fast_fp16=args.fast_fp16)
+    cache = build_cache(args.config, device, seed=1234 + rank, precision=args.precision)
     gen = torch.Generator(device=device)
     gen.manual_seed(99 + rank)
     q = torch.randn(B, Hq, D, device=device, generator=gen)
@@ -356,8 +356,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--fast-fp16", action="store_true",
-                    help="plain fp16 codewords in decode (default: fp16 hi+lo)")
+    ap.add_argument("--precision", default="precise", choices=["precise", "balanced", "fast"],
+                    help="decode codeword precision (DESIGN.md 3.2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     res = run_reference(args) if args.impl == "reference" else run_ours(args)

@@ -175,9 +175,11 @@ typedef struct nsnkv_cache_view {
   const nsnkv_codebook *cb_v;
   int64_t total_chunks;      /* sum of n_chunks (host copy), or -1 to let
                                 the library read it back (synchronises)   */
-  int32_t fast_fp16;         /* 0: codewords as fp16 hi + lo (~22-bit, the
-                                default); 1: plain fp16 codewords (faster,
-                                ~5e-4 relative output error on 2-bit)     */
+  int32_t precision;         /* decode codeword precision: 0 = fp16 hi+lo
+                                on scores and values (~1e-6 relative
+                                output error), 1 = plain fp16 scores, hi+lo
+                                values (~4e-4), 2 = plain fp16 both (~6e-4
+                                on 2-bit; not for 1-bit)   */
 } nsnkv_cache_view;
 
 /* Raw q.K^T of every cached token (quantized chunks first, then residual),

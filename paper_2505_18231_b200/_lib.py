@@ -62,7 +62,7 @@ class CacheView(ctypes.Structure):
         ("cb_k", c_void_p),
         ("cb_v", c_void_p),
         ("total_chunks", c_i64),
-        ("fast_fp16", c_int),
+        ("precision", c_int),
     ]
 
 

@@ -38,6 +38,7 @@ NPAIR = D // 2
 PAGE_BYTES = {BitMode.TWO_BIT: 2304, BitMode.ONE_BIT: 1280}
 LEDGER_BYTES = {BitMode.TWO_BIT: 2292, BitMode.ONE_BIT: 1268}
 CNT_CLAMP, CNT_ZERO, CNT_FALLBACK, CNT_NEARTIE = range(4)
+PRECISIONS = {"precise": 0, "balanced": 1, "fast": 2}
 
 
 class ScaleStrategy(enum.IntEnum):
@@ -142,12 +143,15 @@ class PagedKvCache:
     def __init__(self, config: CacheConfig, batch: int, n_kv_heads: int, max_tokens: int = 0,
                  cb_k: Codebook | None = None, cb_v: Codebook | None = None,
                  base_position: int = 0, device=None, check_finite: bool = True,
-                 fast_fp16: bool = False):
+                 precision: str = "precise"):
         config.check_gpu_path()
         self.check_finite = check_finite
-        # decode precision: False = codewords as fp16 hi + lo (~22 bits, the
-        # default); True = plain fp16 codewords (faster, ~5e-4 relative error)
-        self.fast_fp16 = bool(fast_fp16)
+        # decode codeword precision: "precise" = fp16 hi + lo
+        # on both sides, "balanced" = plain fp16 scores / hi + lo values,
+        # "fast" = plain fp16 both (2-bit only)
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
+        self.precision = precision
         if batch < 1 or n_kv_heads < 1:
             raise ShapeMismatch("batch and n_kv_heads must be >= 1")
         self.config = config
@@ -317,7 +321,7 @@ class PagedKvCache:
         cv.cb_k = cb_k.device_handle(self.device)
         cv.cb_v = cb_v.device_handle(self.device)
         cv.total_chunks = self.units * self.n_chunks
-        cv.fast_fp16 = 1 if self.fast_fp16 else 0
+        cv.precision = PRECISIONS[self.precision]
         return cv
 
     def _q(self, q) -> torch.Tensor:

@@ -156,6 +156,6 @@ int make_cache_view(const nsnkv_cache_view *in, CacheViewDev *out) {
   out->cb_k = in->cb_k->dev;
   out->cb_v = in->cb_v->dev;
   out->total_chunks = in->total_chunks;
-  out->fast_fp16 = in->fast_fp16;
+  out->precision = in->precision;
   return NSNKV_OK;
 }

@@ -232,13 +232,19 @@ __device__ __forceinline__ int k_channel(int t, int kt, int r, int i) {
 // ---------------------------------------------------------------------------
 // the fused kernel
 // ---------------------------------------------------------------------------
-template <int G, bool FOLD, bool HILO>
+// PREC: 0 = codewords fp16 hi + lo on both sides (~1e-6 relative output
+// error), 1 = scores from plain fp16 codewords, values hi + lo (~4e-4; the
+// per-token score rounding is random, the value-side rounding of 1-bit
+// codebooks is systematic), 2 = plain fp16 on both sides (~6e-4 on 2-bit).
+template <int G, bool FOLD, int PREC>
 __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
     attend_kernel(CacheViewDev cv, const float *__restrict__ qg, float *__restrict__ recs,
                   int64_t total_chunks) {
   constexpr int NT = AttCfg<G>::NT;
   constexpr int NGRP = AttCfg<G>::NGRP;
   constexpr int NSTAGE = AttCfg<G>::NSTAGE;
+  constexpr bool HILO_K = PREC == 0;
+  constexpr bool HILO_V = PREC <= 1;
   static_assert(sizeof(AttMisc<G>) <= MISC_LO_MAX, "decode ring does not fit below the tables");
   static_assert(sizeof(AttGroups<G>) <= MISC_HI_MAX, "decode scratch does not fit above the tables");
   extern __shared__ __align__(128) uint8_t smem[];
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
       const uint32_t a0 = prmt(ik0, lbk, sel), a1 = prmt(ik1, lbk, sel);
       uint4 h0 = lds128(a0), h1 = lds128(a1);
       uint4 l0 = make_uint4(0, 0, 0, 0), l1 = l0;
-      if (HILO) {
+      if (HILO_K) {
         l0 = lds128(a0 + 128);
         l1 = lds128(a1 + 128);
       }
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
           const uint32_t w1 = sk1 << (15 - 4 * m - p);
           ph0[p] = xor_sign(ph0[p], w0);
           ph1[p] = xor_sign(ph1[p], w1);
-          if (HILO) {
+          if (HILO_K) {
             pl0[p] = xor_sign(pl0[p], w0);
             pl1[p] = xor_sign(pl1[p], w1);
           }
@@ -580,7 +586,7 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
         // k-tile 2m: pairs 0 (cols 2t..) and 1 (cols 2t+8..); k-tile 2m+1: pairs 2, 3
         mma16816(d1[nt][0], h0.x, h1.x, h0.y, h1.y, qB[nt][2 * m][0], qB[nt][2 * m][1]);
         mma16816(d1[nt][1], h0.z, h1.z, h0.w, h1.w, qB[nt][2 * m + 1][0], qB[nt][2 * m + 1][1]);
-        if (HILO) {
+        if (HILO_K) {
           mma16816(d1[nt][0], l0.x, l1.x, l0.y, l1.y, qB[nt][2 * m][0], qB[nt][2 * m][1]);
           mma16816(d1[nt][1], l0.z, l1.z, l0.w, l1.w, qB[nt][2 * m + 1][0], qB[nt][2 * m + 1][1]);
         }
@@ -668,14 +674,14 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
       for (int q = 0; q < 4; ++q) {
         const uint32_t a = prmt(iv[q], lbv, sel);
         yh[q] = lds128(a);
-        yl[q] = HILO ? lds128(a + 128) : make_uint4(0, 0, 0, 0);
+        yl[q] = HILO_V ? lds128(a + 128) : make_uint4(0, 0, 0, 0);
         if (FOLD) {
           uint32_t *ph = &yh[q].x, *pl = &yl[q].x;
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
             const uint32_t wk = sv[q] << (15 - 4 * sg - p);
             ph[p] = xor_sign(ph[p], wk);
-            if (HILO) pl[p] = xor_sign(pl[p], wk);
+            if (HILO_V) pl[p] = xor_sign(pl[p], wk);
           }
         }
       }
@@ -688,7 +694,7 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
           mma16816(accV[nt][mt], a0h, a1h, a2h, a3h, pf[nt][0], pf[nt][1]);
-        if (HILO) {
+        if (HILO_V) {
           const uint32_t *l0p = &yl[0].x, *l1p = &yl[1].x, *l2p = &yl[2].x, *l3p = &yl[3].x;
           const uint32_t a0l = prmt(l0p[p], l1p[p], 0x5410u), a1l = prmt(l0p[p], l1p[p], 0x7632u);
           const uint32_t a2l = prmt(l2p[p], l3p[p], 0x5410u), a3l = prmt(l2p[p], l3p[p], 0x7632u);
@@ -847,12 +853,12 @@ extern "C" size_t nsnkv_decode_workspace_bytes(const nsnkv_cache_view *cv_in) {
   return a > b ? a : b;
 }
 
-template <int G, bool FOLD, bool HILO>
+template <int G, bool FOLD, int PREC>
 static int launch_attend(const CacheViewDev &cv, const float *q, float *out, float *lse,
                          float *recs, int64_t total, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attend_kernel<G, FOLD, HILO>,
+    cudaFuncSetAttribute(attend_kernel<G, FOLD, PREC>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM_BYTES);
     attr = true;
   }
@@ -860,7 +866,7 @@ static int launch_attend(const CacheViewDev &cv, const float *q, float *out, flo
   if (total < grid) grid = (int)(total > 0 ? total : 1);
   int launches = 1;
   if (total > 0) {
-    attend_kernel<G, FOLD, HILO>
+    attend_kernel<G, FOLD, PREC>
         <<<grid, AttCfg<G>::THREADS, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
     ++launches;
   }
@@ -898,17 +904,20 @@ extern "C" int nsnkv_decode_attend(const nsnkv_cache_view *cv_in, const float *q
   }
   float *recs = (float *)workspace;
   const bool fold = cv.cb_k.bit_mode == 2;
-  const bool hilo = cv.fast_fp16 == 0;
-#define NSNKV_ATT(GG)                                                                    \
-  return fold ? (hilo ? launch_attend<GG, true, true>(cv, q, out, lse, recs, total, st)  \
-                      : launch_attend<GG, true, false>(cv, q, out, lse, recs, total, st)) \
-              : (hilo ? launch_attend<GG, false, true>(cv, q, out, lse, recs, total, st) \
-                      : launch_attend<GG, false, false>(cv, q, out, lse, recs, total, st))
+  const int prec = cv.precision < 0 ? 0 : (cv.precision > 2 ? 2 : cv.precision);
+#define NSNKV_ATT_P(GG, FF)                                                       \
+  return prec == 0 ? launch_attend<GG, FF, 0>(cv, q, out, lse, recs, total, st)  \
+       : prec == 1 ? launch_attend<GG, FF, 1>(cv, q, out, lse, recs, total, st)  \
+                   : launch_attend<GG, FF, 2>(cv, q, out, lse, recs, total, st)
+#define NSNKV_ATT(GG)         \
+  if (fold) NSNKV_ATT_P(GG, true); \
+  else NSNKV_ATT_P(GG, false)
   switch (G) {
     case 1: NSNKV_ATT(1);
     case 2: NSNKV_ATT(2);
     case 4: NSNKV_ATT(4);
     default: NSNKV_ATT(8);
   }
+#undef NSNKV_ATT_P
 #undef NSNKV_ATT
 }

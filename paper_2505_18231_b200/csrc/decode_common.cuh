@@ -18,7 +18,7 @@ struct CacheViewDev {
   int64_t rope_pos0, rope_n;
   CodebookDev cb_k, cb_v;
   int64_t total_chunks;
-  int fast_fp16;
+  int precision;
 };
 
 struct ChunkMeta {

@@ -30,14 +30,15 @@ def _oracle_unit_out(cache, unit, q_unit):
     return out
 
 
-def _build(B, Hkv, T, mode, seed, append_block=4096):
+def _build(B, Hkv, T, mode, seed, append_block=4096, precision="precise"):
     import torch
 
     import paper_2505_18231_b200 as P
 
     cb = P.default_codebook(mode)
     cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
-    cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, check_finite=False)
+    cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, check_finite=False,
+                           precision=precision)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
     done = 0
@@ -49,17 +50,21 @@ def _build(B, Hkv, T, mode, seed, append_block=4096):
     return cache
 
 
-@pytest.mark.parametrize("mode,B,Hq,Hkv,T", [
-    ("2b", 16, 32, 8, 32768),      # BASELINE config 2 (headline)
-    ("1b", 4, 32, 8, 8192 + 37),   # 1-bit with a residual tail
-    ("2b", 2, 8, 8, 4096 + 5),     # G = 1 (config 1 geometry)
-    ("2b", 3, 16, 2, 1000),        # G = 8, ragged
-    ("1b", 2, 4, 2, 64 * 3),       # G = 2
+@pytest.mark.parametrize("mode,B,Hq,Hkv,T,precision", [
+    ("2b", 16, 32, 8, 32768, "precise"),    # BASELINE config 2 (headline)
+    ("2b", 16, 32, 8, 32768, "balanced"),
+    ("2b", 16, 32, 8, 32768, "fast"),
+    ("1b", 4, 32, 8, 32768 + 37, "precise"),  # 1-bit with a residual tail
+    ("1b", 4, 32, 8, 32768 + 37, "balanced"),
+    ("2b", 2, 8, 8, 4096 + 5, "precise"),   # G = 1 (config 1 geometry)
+    ("1b", 1, 8, 8, 4096, "balanced"),      # config 1 itself
+    ("2b", 3, 16, 2, 1000, "precise"),      # G = 8, ragged
+    ("1b", 2, 4, 2, 64 * 3, "precise"),     # G = 2
 ])
-def test_fused_decode_vs_oracle(mode, B, Hq, Hkv, T):
+def test_fused_decode_vs_oracle(mode, B, Hq, Hkv, T, precision):
     import torch
 
-    cache = _build(B, Hkv, T, mode, seed=T + B)
+    cache = _build(B, Hkv, T, mode, seed=T + B, precision=precision)
     g = torch.Generator(device="cuda")
     g.manual_seed(5)
     q = torch.randn(B, Hq, 128, device="cuda", generator=g)
@@ -69,13 +74,16 @@ def test_fused_decode_vs_oracle(mode, B, Hq, Hkv, T):
     units = [0, B * Hkv - 1] if B * Hkv > 1 else [0]
     if B * Hkv > 4:
         units.append((B * Hkv) // 2 + 1)
+    worst = 0.0
     for u in units:
         b, h = divmod(u, Hkv)
         ref = _oracle_unit_out(cache, u, qn[b, h * G:(h + 1) * G])
         got = out[b, h * G:(h + 1) * G]
         for i in range(G):
             err = np.max(np.abs(got[i] - ref[i])) / np.max(np.abs(ref[i]))
+            worst = max(worst, err)
             assert err <= TOL, f"unit {u} head {i}: rel err {err:.2e}"
+    print(f"[{mode} {precision} T={T} G={G}] worst max-rel error {worst:.2e}")
     assert np.isfinite(out).all()
 
 
