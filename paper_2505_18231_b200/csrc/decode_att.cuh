@@ -1,0 +1,264 @@
+// decode_att.cuh -- PTX helpers, chunk cursor, stream-K records and the
+// combine kernel shared by the decode kernels (decode_attend.cu, decode_ws.cu).
+#pragma once
+#include "common.cuh"
+#include "decode_common.cuh"
+
+namespace nsnkv {
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// x ^ (w & 0x80008000): flip the fp16 sign bits selected by bits 15 / 31 of w
+// in one LOP3
+__device__ __forceinline__ uint32_t xor_sign(uint32_t x, uint32_t w) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(r) : "r"(x), "r"(w), "r"(0x80008000u));
+  return r;
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo16, float hi16) {
+  const __half2 h = __floats2half2_rn(lo16, hi16);
+  return *reinterpret_cast<const uint32_t *>(&h);
+}
+// x = hi + lo with hi = fp16(x), lo = fp16(x - hi)
+__device__ __forceinline__ void split_h(float x, float &hi, float &lo) {
+  hi = __half2float(__float2half_rn(x));
+  lo = x - hi;
+}
+
+// ---------------------------------------------------------------------------
+// configuration
+// ---------------------------------------------------------------------------
+constexpr int ROPE_ROW_BYTES = NPAIR * 8;        // 64 x (cos, sin) fp32
+constexpr int STAGE_BYTES = 2 * NSNKV_PAGE_BYTES_2B + ROPE_ROW_BYTES;
+constexpr int ATT_SMEM_BYTES = 232448;           // 227 KB: two 64 KB-aligned tables + misc
+constexpr int MISC_LO_MAX = 65536 - 1024;        // below the tables (1 KB is reserved)
+constexpr int MISC_HI_MAX = 232448 + 1024 - 196608;  // above the tables
+constexpr float LOG2E_OVER_SQRTD = 1.4426950408889634f * 0.08838834764831845f;
+
+struct ChunkCursor {
+  int u, c, n;  // unit, chunk within unit, chunks of the unit
+};
+
+__device__ __forceinline__ void cursor_advance(ChunkCursor &cur, const int32_t *n_chunks,
+                                               int n_units) {
+  if (++cur.c >= cur.n) {
+    cur.c = 0;
+    cur.n = 0;
+    while (cur.n == 0 && ++cur.u < n_units) cur.n = n_chunks[cur.u];
+  }
+}
+
+// Warp-parallel seek of global chunk x (all 32 lanes call; every lane gets
+// the result).  Units with zero chunks are skipped.
+__device__ __forceinline__ ChunkCursor cursor_seek(int64_t x, const int32_t *n_chunks,
+                                                   int n_units) {
+  const int lane = threadIdx.x & 31;
+  int64_t acc = 0;
+  for (int base = 0; base < n_units; base += 32) {
+    const int u = base + lane;
+    const int64_t n = u < n_units ? n_chunks[u] : 0;
+    int64_t incl = n;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, n > 0 && acc + incl > x);
+    if (hit) {
+      const int L = __ffs(hit) - 1;
+      const int64_t excl = __shfl_sync(0xffffffffu, incl - n, L);
+      const int nn = (int)__shfl_sync(0xffffffffu, n, L);
+      return ChunkCursor{base + L, (int)(x - acc - excl), nn};
+    }
+    acc += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return ChunkCursor{n_units, 0, 0};
+}
+
+__host__ __device__ __forceinline__ int64_t range_lo(int64_t total, int i, int grid) {
+  return total * i / grid;
+}
+
+// record layout: [slot][G][4 + D]: m (log2 domain), l, -, -, acc[128] (HT
+// domain); slot = (unit + cta) * NGRP + group.
+template <int G>
+__device__ __forceinline__ float *record_ptr(float *recs, int slot) {
+  return recs + (int64_t)slot * G * (4 + D);
+}
+
+// channel of the K-side MMA k-index (thread t, k-tile kt, column group r,
+// element i): thread t owns the whole sub-vectors 4t..4t+3 of each token.
+__device__ __forceinline__ int k_channel(int t, int kt, int r, int i) {
+  return 32 * t + 8 * (kt >> 1) + 4 * (kt & 1) + 2 * r + i;
+}
+
+// ---------------------------------------------------------------------------
+// combine: merge the stream-K records of a unit with its exact residual rows,
+// normalise, inverse FWHT (attention.py:105-108, 129-133, 141).
+// One CTA (128 threads) per (batch, q-head).
+// ---------------------------------------------------------------------------
+template <int G, int NGRP>
+__global__ void __launch_bounds__(128) combine_kernel(CacheViewDev cv, const float *__restrict__ qg,
+                                                      const float *__restrict__ recs,
+                                                      int64_t total_chunks, int grid,
+                                                      float *__restrict__ out,
+                                                      float *__restrict__ lse) {
+  __shared__ float s_acc[D];
+  __shared__ float s_w[R];
+  __shared__ float s_q[D];
+  __shared__ int64_t s_red[128];
+  const int row = blockIdx.x;
+  const int b = row / cv.n_q_heads, i = row - b * cv.n_q_heads;
+  const int hk = i / G, h = i - hk * G;
+  const int u = b * cv.n_kv_heads + hk;
+  const int ch = threadIdx.x;
+  {
+    int64_t acc = 0;
+    for (int uu = ch; uu < u; uu += 128) acc += cv.n_chunks[uu];
+    s_red[ch] = acc;
+  }
+  s_q[ch] = qg[(int64_t)row * D + ch];
+  __syncthreads();
+  for (int off = 64; off > 0; off >>= 1) {
+    if (ch < off) s_red[ch] += s_red[ch + off];
+    __syncthreads();
+  }
+  const int64_t s_off = s_red[0];
+  const int nch = cv.n_chunks[u];
+  float m = -INFINITY, l = 0.f, a = 0.f;
+  if (nch > 0) {
+    const int64_t x0 = s_off, x1 = s_off + nch - 1;
+    int c0 = (int)(x0 * grid / total_chunks);
+    while (c0 + 1 < grid && range_lo(total_chunks, c0 + 1, grid) <= x0) ++c0;
+    while (c0 > 0 && range_lo(total_chunks, c0, grid) > x0) --c0;
+    int c1 = (int)(x1 * grid / total_chunks);
+    while (c1 + 1 < grid && range_lo(total_chunks, c1 + 1, grid) <= x1) ++c1;
+    while (c1 > 0 && range_lo(total_chunks, c1, grid) > x1) --c1;
+    for (int c = c0; c <= c1; ++c) {
+      // local chunk indices of unit u inside CTA c; group gq owns k % NGRP == gq
+      const int64_t clo = range_lo(total_chunks, c, grid);
+      const int64_t chi = range_lo(total_chunks, c + 1, grid);
+      const int64_t ka = (x0 > clo ? x0 : clo) - clo;
+      const int64_t kb = (x1 + 1 < chi ? x1 + 1 : chi) - clo;
+      for (int gq = 0; gq < NGRP; ++gq) {
+        if (!(ka + ((gq - ka % NGRP + NGRP) % NGRP) < kb)) continue;
+        const float *rec = record_ptr<G>(const_cast<float *>(recs), (u + c) * NGRP + gq) + h * (4 + D);
+        const float rm = rec[0], rl = rec[1];
+        if (!(rm > -INFINITY)) continue;  // the group saw no chunk of this unit
+        const float mn = fmaxf(m, rm);
+        const float sa = exp2f(m - mn), sb = exp2f(rm - mn);
+        a = a * sa + rec[4 + ch] * sb;
+        l = l * sa + rl * sb;
+        m = mn;
+      }
+    }
+  }
+  // residual rows: exact RoPE(k, pos) . q scores (base-2 logits)
+  const int nres = cv.n_res[u];
+  if (nres > 0) {
+    const int64_t pbase = cv.base_pos[u] + (int64_t)nch * R;
+    if (ch < nres) {
+      const float *kr = cv.k_res + ((int64_t)u * R + ch) * D;
+      const float2 *cs = cv.rope_cs + (pbase + ch - cv.rope_pos0) * NPAIR;
+      float acc = 0.f;
+      for (int j = 0; j < NPAIR; ++j) {
+        const float2 e = cs[j];
+        const float ke = kr[2 * j], ko = kr[2 * j + 1];
+        acc = fmaf(ke * e.x - ko * e.y, s_q[2 * j], acc);
+        acc = fmaf(ke * e.y + ko * e.x, s_q[2 * j + 1], acc);
+      }
+      s_w[ch] = acc * LOG2E_OVER_SQRTD;
+    }
+    __syncthreads();
+    float rm = -INFINITY;
+    for (int tt = 0; tt < nres; ++tt) rm = fmaxf(rm, s_w[tt]);
+    const float mn = fmaxf(m, rm);
+    const float sa = (m > -INFINITY) ? exp2f(m - mn) : 0.f;
+    a *= sa;
+    l *= sa;
+    for (int tt = 0; tt < nres; ++tt) {
+      const float p = exp2f(s_w[tt] - mn);
+      l += p;
+      a = fmaf(p, cv.v_res[((int64_t)u * R + tt) * D + ch], a);
+    }
+    m = mn;
+  }
+  s_acc[ch] = (l > 0.f) ? a / l : 0.f;
+  __syncthreads();
+  block_fwht128(s_acc);
+  out[(int64_t)row * D + ch] = s_acc[ch];
+  if (lse && ch == 0) lse[row] = (l > 0.f) ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
+}
+
+
+}  // namespace nsnkv
+
+// warp-specialized decode launcher (decode_ws.cu), instantiated for G = 1, 2, 4
+template <int G, bool FOLD, int PREC>
+int nsnkv_launch_attend_ws(const nsnkv::CacheViewDev &cv, const float *q, float *out, float *lse,
+                           float *recs, int64_t total, int grid, cudaStream_t st);
