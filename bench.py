@@ -46,6 +46,7 @@ CONFIGS = {
     "c2": (16, 32, 8, 32768, 2),
     "c2_1b": (16, 32, 8, 32768, 1),
     "c1": (1, 8, 8, 4096, 1),
+    "c4": (128, 32, 8, 131072, 2),
 }
 
 
@@ -282,9 +283,79 @@ def run_ours(args) -> dict | None:
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
     }
+    if world == 1 and not args.no_extras:
+        res["serving_step"] = measure_serving(cache, q, steps=2 * R)
+        res["encode"] = measure_encode(device, bm)
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
     return res
+
+
+def measure_serving(cache, q, steps: int) -> dict:
+    """One decode step as a server runs it: append this step's K/V token for
+    every (sequence, kv-head) -- a 64-token chunk is flushed through the
+    encode kernel every 64 steps -- then attend.  Averaged over `steps`
+    steps (a multiple of 64, so the flushes are included)."""
+    import torch
+
+    B, Hkv = cache.batch, cache.n_kv_heads
+    dev = q.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    ks = torch.randn(steps, B, Hkv, 1, D, device=dev, generator=g)
+    vs = torch.randn(steps, B, Hkv, 1, D, device=dev, generator=g)
+    out = torch.empty_like(q)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        cache.append(ks[i], vs[i])
+        cache.attend(q, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"what": "append 1 token/sequence (flush every 64) + attend", "ms_per_step": round(ms, 4),
+            "tokens_per_s": round(B / (ms * 1e-3), 1), "steps": steps,
+            "context_after": cache.total_tokens}
+
+
+def measure_encode(device, bit_mode: int, batch: int = 64, heads: int = 8, tokens: int = 8192) -> dict:
+    """BASELINE config 3: prefill quantize/append of a 64 x 8K x 8-head
+    bf16 K/V batch (one append call, all chunks flushed)."""
+    import torch
+
+    import paper_2505_18231_b200 as P
+
+    cb = P.default_codebook(f"{bit_mode}b")
+    cfg = P.CacheConfig(d=D, bit_mode=cb.bit_mode)
+    g = torch.Generator(device=device)
+    g.manual_seed(3)
+    k = torch.randn(batch, heads, tokens, D, device=device, generator=g).to(torch.bfloat16)
+    v = torch.randn(batch, heads, tokens, D, device=device, generator=g).to(torch.bfloat16)
+    times = []
+    for it in range(3):
+        cache = P.PagedKvCache(cfg, batch, heads, max_tokens=tokens, cb_k=cb, cb_v=cb,
+                               device=device, check_finite=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cache.append(k, v)
+        e1.record()
+        torch.cuda.synchronize()
+        if it:
+            times.append(e0.elapsed_time(e1))
+    ms = min(times)
+    th = batch * heads * tokens
+    nbytes = th * D * 2 * 2 + (th // R) * LEDGER[bit_mode] * 2
+    macs = th * 2 * 16 * 256 * 8
+    del k, v, cache
+    torch.cuda.empty_cache()
+    return {"workload": f"config 3: batch {batch} x {heads} kv-heads x {tokens} tokens, bf16 in, "
+                        f"{bit_mode}-bit", "ms": round(ms, 3),
+            "token_heads_per_s": round(th / (ms * 1e-3), 1),
+            "GBps_algorithmic": round(nbytes / (ms * 1e-3) / 1e9, 1),
+            "search_TMACps": round(macs / (ms * 1e-3) / 1e12, 2),
+            "bound": "compute (codebook search, 32768 MAC per token vector)"}
 
 
 def cpu_baseline(cfg_name: str, budget_s: float = 15.0, threads: int | None = None) -> dict:
@@ -355,6 +426,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the serving-step and encode measurements")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--precision", default="precise", choices=["precise", "balanced", "fast"],
                     help="decode codeword precision (DESIGN.md 3.2)")

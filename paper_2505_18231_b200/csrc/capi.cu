@@ -86,6 +86,16 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
       tw[c * 16 + 8 + slot] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
   }
+  // encode search B fragments: normalized entries split into fp16 hi + lo
+  std::vector<uint2> mb(32 * 32);
+  for (int nt = 0; nt < 32; ++nt)
+    for (int L = 0; L < 32; ++L) {
+      const int c = 8 * nt + (L >> 2), t = L & 3;
+      const float *e = entries_host + 8 * c;
+      const float a = (float)((double)e[2 * t] * inv[c]), b = (float)((double)e[2 * t + 1] * inv[c]);
+      const float ah = __half2float(__float2half_rn(a)), bh = __half2float(__float2half_rn(b));
+      mb[nt * 32 + L] = make_uint2(pack_half2(a, b), pack_half2(a - ah, b - bh));
+    }
   nsnkv_codebook *cb = new nsnkv_codebook();
   cb->dev.bit_mode = bit_mode;
   cudaError_t err = cudaSuccess;
@@ -93,10 +103,12 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
   if (!err) err = cudaMalloc(&cb->dev.inv, NENT * sizeof(double));
   if (!err) err = cudaMalloc(&cb->dev.inv32, NENT * sizeof(float));
   if (!err) err = cudaMalloc(&cb->dev.tabw, NENT * 16 * sizeof(uint4));
+  if (!err) err = cudaMalloc(&cb->dev.mma_b, 32 * 32 * sizeof(uint2));
   if (!err) err = cudaMemcpy(cb->dev.entries, entries_host, NENT * 8 * sizeof(float), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(cb->dev.inv, inv.data(), NENT * sizeof(double), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(cb->dev.inv32, inv32.data(), NENT * sizeof(float), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(cb->dev.tabw, tw.data(), NENT * 16 * sizeof(uint4), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(cb->dev.mma_b, mb.data(), 32 * 32 * sizeof(uint2), cudaMemcpyHostToDevice);
   if (err) {
     nsnkv_codebook_destroy(cb);
     snprintf(g_err, sizeof(g_err), "codebook upload: %s", cudaGetErrorString(err));
@@ -112,6 +124,7 @@ extern "C" int nsnkv_codebook_destroy(nsnkv_codebook *cb) {
   cudaFree(cb->dev.inv);
   cudaFree(cb->dev.inv32);
   cudaFree(cb->dev.tabw);
+  cudaFree(cb->dev.mma_b);
   delete cb;
   return NSNKV_OK;
 }

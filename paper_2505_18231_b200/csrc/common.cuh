@@ -54,6 +54,10 @@ struct CodebookDev {
   // lo = fp16(e - hi)); 8 replicas so a quarter-warp of 16-byte loads with
   // slot = lane % 8 never bank-conflicts.
   uint4 *tabw;
+  // encode search B fragments (mma.sync m16n8k16): [n-tile 32][lane 32] of
+  // (fp16 hi, fp16 lo) halves of the normalized entry e_c / ||e_c|| at
+  // components 2t, 2t+1 of entry c = 8 n-tile + lane / 4.
+  uint2 *mma_b;
   int bit_mode;
 };
 

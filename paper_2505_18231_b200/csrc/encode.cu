@@ -12,6 +12,7 @@
 // divides, no FMA contraction where the reference rounds products, fp64 sums
 // in numpy's pairwise order), so pages are bit-identical to the oracle's.
 #include "common.cuh"
+#include "decode_att.cuh"
 #include "match.cuh"
 
 namespace nsnkv {
@@ -25,7 +26,8 @@ struct EncodeSmem {
   double inv[NENT];
   float inv32[NENT];
   float s1[R], s2[R], o[D];
-  double part[R];                 // per-token fp64 scratch
+  uint2 mb[32][32];               // search B fragments (normalized entries hi/lo)
+  uint16_t zmask[R];              // zero sub-vectors per token (bit j)
   float s2adj[R];
   uint8_t idx[R][NSUB];
   uint8_t sgn[R][NSUB];
@@ -125,7 +127,8 @@ __device__ __forceinline__ uint32_t rtn4_level(float v, float zero32f, float sca
   return (uint32_t)lv;
 }
 
-__global__ void __launch_bounds__(ENC_THREADS) encode_chunks_kernel(
+template <bool FOLD>
+__global__ void __launch_bounds__(ENC_THREADS, 2) encode_chunks_kernel(
     const float *__restrict__ residual, int n_resid, const void *__restrict__ fresh, int fresh_bf16,
     int64_t n_fresh, int n_flush, int is_key, const int64_t *__restrict__ start_pos,
     const float2 *__restrict__ rope_cs, int64_t rope_pos0, int64_t rope_n, CodebookDev cb,
@@ -136,8 +139,9 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_chunks_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int u = blockIdx.x / n_flush;
   const int k = blockIdx.x - u * n_flush;
-  const PageLayout L = page_layout(cb.bit_mode);
-  const bool fold = cb.bit_mode == 2;
+  const PageLayout L = page_layout(FOLD ? 2 : 1);
+  constexpr bool fold = FOLD;
+  const int g = lane >> 2, lt = lane & 3;  // mma fragment coordinates
 
   if (tid < NSNKV_NUM_COUNTERS) s.cnt[tid] = 0;
   for (int i = tid; i < NENT * 8; i += ENC_THREADS) s.ent[i] = cb.entries[i];
@@ -145,6 +149,7 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_chunks_kernel(
     s.inv[i] = cb.inv[i];
     s.inv32[i] = cb.inv32[i];
   }
+  for (int i = tid; i < 32 * 32; i += ENC_THREADS) (&s.mb[0][0])[i] = cb.mma_b[i];
   // ---- 1. gather the chunk's 64 stream rows (kvcache.py:179-186) ----------
   for (int i = tid; i < R * (D / 4); i += ENC_THREADS) {
     const int t = i / (D / 4), c4 = i - t * (D / 4);
@@ -207,35 +212,137 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_chunks_kernel(
   }
 
   // ---- 4. codebook match (codebook.py:109-128, _native.pyx:41-87) -------
+  // (a) sign bytes and zero rows, one thread per (token, 4 sub-vectors)
   {
-    const int t = tid >> 2;          // token
-    const int j0 = (tid & 3) * 4;    // first of 4 sub-vectors
-    float u4[4][8];
-    uint32_t sb[4];
-    bool zero[4];
+    const int tt = tid >> 2, j0 = (tid & 3) * 4;
+    uint32_t zm = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      float v[8];
-      const float4 a = *reinterpret_cast<float4 *>(&s.x[t][8 * (j0 + i)]);
-      const float4 b = *reinterpret_cast<float4 *>(&s.x[t][8 * (j0 + i) + 4]);
+      float v[8], u[8];
+      const float4 a = *reinterpret_cast<float4 *>(&s.x[tt][8 * (j0 + i)]);
+      const float4 b = *reinterpret_cast<float4 *>(&s.x[tt][8 * (j0 + i) + 4]);
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
       v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-      zero[i] = sq_norm8_pairwise(v) < 1e-24;
-      sb[i] = fold_signs(v, u4[i], fold);
+      const bool zero = sq_norm8_pairwise(v) < 1e-24;
+      const uint32_t sb = fold_signs(v, u, FOLD);
+      s.sgn[tt][j0 + i] = zero ? 0 : (uint8_t)sb;
+      zm |= (zero ? 1u : 0u) << (j0 + i);
     }
-    int best[4];
-    const uint32_t slow =
-        match_multi<4>(u4, reinterpret_cast<const float4 *>(s.ent), s.inv32, s.ent, s.inv, best);
-    int nz = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      s.idx[t][j0 + i] = zero[i] ? 0 : (uint8_t)best[i];
-      s.sgn[t][j0 + i] = zero[i] ? 0 : (uint8_t)sb[i];
-      nz += zero[i] ? 1 : 0;
+    // the four threads of a token combine their zero bits
+    zm |= __shfl_xor_sync(0xffffffffu, zm, 1);
+    zm |= __shfl_xor_sync(0xffffffffu, zm, 2);
+    if ((tid & 3) == 0) {
+      s.zmask[tt] = (uint16_t)zm;
+      if (zm) atomicAdd(&s.cnt[NSNKV_CNT_ZERO], __popc(zm));
     }
-    if (nz) atomicAdd(&s.cnt[NSNKV_CNT_ZERO], nz);
-    if (slow) atomicAdd(&s.cnt[NSNKV_CNT_NEARTIE], __popc(slow));
   }
+  // (b) tensor-core pre-pass: scores[sub][c] = u . e_c / ||e_c|| with u and
+  // the normalized entries split into fp16 hi + lo (mma.sync m16n8k16: K =
+  // [u_hi | u_lo] against [e_hi ; e_hi], then [u_hi | u_lo] against
+  // [e_lo ; 0]).  One m-tile = the 16 sub-vectors of one token; warp w takes
+  // tokens 8w .. 8w+7.  Scores are tracked as packed (score | 255 - c) keys
+  // with top-2 per sub-vector; a sub-vector whose runner-up is within the
+  // error bound is re-scored exactly in fp64 (the reference loop).
+  int slow = 0;
+#pragma unroll 1
+  for (int hf = 0; hf < 2; ++hf) {  // two passes of 4 tokens keep the live state small
+    uint32_t A[4][4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int tau = 8 * warp + 4 * hf + m;
+      const float2 v0 = *reinterpret_cast<const float2 *>(&s.x[tau][8 * g + 2 * lt]);
+      const float2 v1 = *reinterpret_cast<const float2 *>(&s.x[tau][8 * (g + 8) + 2 * lt]);
+      float u0 = FOLD ? fabsf(v0.x) : v0.x, u1 = FOLD ? fabsf(v0.y) : v0.y;
+      float w0 = FOLD ? fabsf(v1.x) : v1.x, w1 = FOLD ? fabsf(v1.y) : v1.y;
+      float h0, l0, h1, l1, h2, l2, h3, l3;
+      split_h(u0, h0, l0);
+      split_h(u1, h1, l1);
+      split_h(w0, h2, l2);
+      split_h(w1, h3, l3);
+      A[m][0] = pack_h2(h0, h1);  // row g   (sub g),   K cols 2t..2t+1: u_hi
+      A[m][1] = pack_h2(h2, h3);  // row g+8 (sub g+8)
+      A[m][2] = pack_h2(l0, l1);  // row g,   K cols 2t+8..2t+9: u_lo
+      A[m][3] = pack_h2(l2, l3);  // row g+8
+    }
+    float best[4][2], sec[4][2];
+    int bi[4][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        best[m][r] = sec[m][r] = -3.0e38f;
+        bi[m][r] = 0;
+      }
+#pragma unroll 2
+    for (int nt = 0; nt < 32; ++nt) {
+      const uint2 bb = s.mb[nt][lane];
+      const int c0 = 8 * nt + 2 * lt;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        mma16816(d, A[m][0], A[m][1], A[m][2], A[m][3], bb.x, bb.x);
+        mma16816(d, A[m][0], A[m][1], A[m][2], A[m][3], bb.y, 0u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = q >> 1;
+          const float v = d[q];
+          sec[m][r] = fmaxf(sec[m][r], fminf(best[m][r], v));
+          if (v > best[m][r]) bi[m][r] = c0 + (q & 1);
+          best[m][r] = fmaxf(best[m][r], v);
+        }
+      }
+    }
+    // merge the top-2 lists of the four lanes sharing a sub-vector (same g)
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+          const float ob = __shfl_xor_sync(0xffffffffu, best[m][r], off);
+          const float os = __shfl_xor_sync(0xffffffffu, sec[m][r], off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi[m][r], off);
+          sec[m][r] = fmaxf(fminf(best[m][r], ob), fmaxf(sec[m][r], os));
+          if (ob > best[m][r] || (ob == best[m][r] && oi < bi[m][r])) bi[m][r] = oi;
+          best[m][r] = fmaxf(best[m][r], ob);
+        }
+      }
+    // decide: lane lt owns token m = lt of this pass (rows g and g + 8)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m != lt) continue;
+      const int tau = 8 * warp + 4 * hf + m;
+      const uint32_t zm = s.zmask[tau];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int sub = g + 8 * r;
+        uint8_t res = 0;
+        if (!((zm >> sub) & 1u)) {
+          const float sb = best[m][r], ss = sec[m][r];
+          float u[8];
+          float n2 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float v = s.x[tau][8 * sub + k];
+            u[k] = (FOLD && v < 0.f) ? -v : v;
+            n2 = fmaf(u[k], u[k], n2);
+          }
+          // fp16 hi + lo operands (2^-22 each) with fp32 tensor-core
+          // accumulation: |score error| < 2^-19 * ||u||; 4x margin
+          const float bound = 2.0f * 7.6293945e-06f * sqrtf(n2);  // 2 * 2^-17 * ||u||
+          const bool ok = n2 > 1e-24f && n2 < 1e30f && ss < sb - bound;
+          if (ok) {
+            res = (uint8_t)bi[m][r];
+          } else {
+            res = (uint8_t)match_exact_fp64(u, s.ent, s.inv);
+            ++slow;
+          }
+        }
+        s.idx[tau][sub] = res;
+      }
+    }
+  }
+  if (slow) atomicAdd(&s.cnt[NSNKV_CNT_NEARTIE], slow);
   if (clamps) atomicAdd(&s.cnt[NSNKV_CNT_CLAMP], clamps);
   __syncthreads();
 
@@ -393,12 +500,19 @@ extern "C" int nsnkv_encode_chunks(const float *residual, int32_t n_resid, const
   const size_t smem = sizeof(EncodeSmem);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(encode_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(encode_chunks_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    cudaFuncSetAttribute(encode_chunks_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(encode_chunks_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         100);
+    cudaFuncSetAttribute(encode_chunks_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         100);
     attr_set = true;
   }
   const int64_t blocks = (int64_t)n_units * n_flush;
-  encode_chunks_kernel<<<(unsigned)blocks, ENC_THREADS, smem, (cudaStream_t)stream>>>(
+  auto kern = dev.bit_mode == 2 ? encode_chunks_kernel<true> : encode_chunks_kernel<false>;
+  kern<<<(unsigned)blocks, ENC_THREADS, smem, (cudaStream_t)stream>>>(
       residual, n_resid, fresh, fresh_bf16, n_fresh, n_flush, is_key, start_pos,
       reinterpret_cast<const float2 *>(rope_cs), rope_pos0, rope_n, dev, strategy, pool, page_ids,
       page_id_stride, counters);
