@@ -235,6 +235,8 @@ __global__ void __launch_bounds__(ENC_THREADS, 2) encode_chunks_kernel(
       s.zmask[tt] = (uint16_t)zm;
       if (zm) atomicAdd(&s.cnt[NSNKV_CNT_ZERO], __popc(zm));
     }
+    // token tt belongs to warp tt / 8, which also decides its sub-vectors below
+    __syncwarp();
   }
   // (b) tensor-core pre-pass: scores[sub][c] = u . e_c / ||e_c|| with u and
   // the normalized entries split into fp16 hi + lo (mma.sync m16n8k16: K =
