@@ -65,7 +65,7 @@ struct AttGroup {
     Chunk ck;
     Merge mg;
   };
-  float q[G][D];              // RoPE'd q of the group's current unit
+  float q[G][D + 4];          // RoPE'd q of the group's current unit (padded: banks)
 };
 
 // Stage ring, constant shift-term fragments and barriers (below the 64
@@ -128,15 +128,29 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
   if (lo >= hi) return;
 
   // stage loader: chunk k of the CTA range goes to stage k % NSTAGE
-  auto load_chunk = [&](int k, const ChunkCursor &c) {
+  // page id and RoPE row of a chunk (global loads; the refilling leader
+  // fetches them one iteration ahead)
+  auto chunk_src = [&](const ChunkCursor &c, int64_t &page, int64_t &p0) {
+    if (c.u < n_units) {
+      page = cv.page_table[(int64_t)c.u * cv.page_table_stride + c.c];
+      p0 = cv.base_pos[c.u] + (int64_t)c.c * R - cv.rope_pos0;
+    } else {
+      page = 0;
+      p0 = 0;
+    }
+  };
+  auto load_chunk_src = [&](int k, int64_t page, int64_t p0) {
     const int s = k % NSTAGE;
-    const int64_t page = cv.page_table[(int64_t)c.u * cv.page_table_stride + c.c];
-    const int64_t p0 = cv.base_pos[c.u] + (int64_t)c.c * R - cv.rope_pos0;
     uint8_t *st = M.st[s];
     mbar_expect_tx(&M.full[s], 2 * page_bytes + ROPE_ROW_BYTES);
     tma_load_1d(st, cv.k_pool + page * page_bytes, page_bytes, &M.full[s]);
     tma_load_1d(st + page_bytes, cv.v_pool + page * page_bytes, page_bytes, &M.full[s]);
     tma_load_1d(st + 2 * page_bytes, cv.rope_cs + p0 * NPAIR, ROPE_ROW_BYTES, &M.full[s]);
+  };
+  auto load_chunk = [&](int k, const ChunkCursor &c) {
+    int64_t page, p0;
+    chunk_src(c, page, p0);
+    load_chunk_src(k, page, p0);
   };
   const int n_local = (int)(hi - lo);
 
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
   auto setup_unit = [&](int unit) {
     const int b = unit / cv.n_kv_heads, hk = unit - b * cv.n_kv_heads;
     const float *qs = qg + ((int64_t)b * cv.n_q_heads + (int64_t)hk * G) * D;
-    for (int i = ci; i < G * D; i += 128) S.q[i / D][i % D] = qs[i];
+    for (int i = ci; i < G * D; i += 128) S.q[i / D][i % D] = qs[i];  // padded rows
     named_bar(bar_id, 128);
     for (int h = ws; h < G; h += 4) {  // HT(q), 4 values per lane
       float4 v = *reinterpret_cast<float4 *>(&S.q[h][4 * lane]);
@@ -313,6 +327,8 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
   // i - NGRP + NSTAGE, issued once the prologue barrier of chunk i shows every
   // warp of the group past chunk i - NGRP
   ChunkCursor ahead = cursor_seek(lo + NSTAGE + grp, cv.n_chunks, n_units);
+  int64_t ahead_page = 0, ahead_p0 = 0;  // prefetched source of the next refill
+  if (leader) chunk_src(ahead, ahead_page, ahead_p0);
   int cur_unit = -1;
   bool tabs_ready = false;
   int nloc = 0;  // chunks processed by this group (prologue slot parity)
@@ -392,10 +408,11 @@ __global__ void __launch_bounds__(AttCfg<G>::THREADS, 1)
     if (i >= NGRP) {
       if (leader) {  // every warp of the group is past chunk i - NGRP
         mbar_wait(&M.pro[grp][slot], pro_parity);
-        if (i - NGRP + NSTAGE < n_local) load_chunk(i - NGRP + NSTAGE, ahead);
+        if (i - NGRP + NSTAGE < n_local) load_chunk_src(i - NGRP + NSTAGE, ahead_page, ahead_p0);
       }
 #pragma unroll
       for (int a2 = 0; a2 < NGRP; ++a2) cursor_advance(ahead, cv.n_chunks, n_units);
+      if (leader) chunk_src(ahead, ahead_page, ahead_p0);  // consumed next iteration
     }
 
     // ---- K side: payload dot products on tensor cores ------------------------
