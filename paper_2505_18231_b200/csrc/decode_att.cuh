@@ -160,39 +160,33 @@ __device__ __forceinline__ int k_channel(int t, int kt, int r, int i) {
 // ---------------------------------------------------------------------------
 // combine: merge the stream-K records of a unit with its exact residual rows,
 // normalise, inverse FWHT (attention.py:105-108, 129-133, 141).
-// One CTA (128 threads) per (batch, q-head).
+// One warp per (batch, q-head); lane l owns channels 4l .. 4l+3.
 // ---------------------------------------------------------------------------
+constexpr int COMBINE_ROWS = 4;  // warps (rows) per CTA
+
 template <int G, int NGRP>
-__global__ void __launch_bounds__(128) combine_kernel(CacheViewDev cv, const float *__restrict__ qg,
-                                                      const float *__restrict__ recs,
-                                                      int64_t total_chunks, int grid,
-                                                      float *__restrict__ out,
-                                                      float *__restrict__ lse) {
-  __shared__ float s_acc[D];
-  __shared__ float s_w[R];
-  __shared__ float s_q[D];
-  __shared__ int64_t s_red[128];
-  const int row = blockIdx.x;
+__global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
+    CacheViewDev cv, const float *__restrict__ qg, const float *__restrict__ recs,
+    int64_t total_chunks, int grid, float *__restrict__ out, float *__restrict__ lse) {
+  __shared__ __align__(16) float s_q[COMBINE_ROWS][D];
+  __shared__ float s_w[COMBINE_ROWS][R];
+  const int wr = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * COMBINE_ROWS + wr;
+  if (row >= cv.batch * cv.n_q_heads) return;
   const int b = row / cv.n_q_heads, i = row - b * cv.n_q_heads;
   const int hk = i / G, h = i - hk * G;
   const int u = b * cv.n_kv_heads + hk;
-  const int ch = threadIdx.x;
-  {
-    int64_t acc = 0;
-    for (int uu = ch; uu < u; uu += 128) acc += cv.n_chunks[uu];
-    s_red[ch] = acc;
-  }
-  s_q[ch] = qg[(int64_t)row * D + ch];
-  __syncthreads();
-  for (int off = 64; off > 0; off >>= 1) {
-    if (ch < off) s_red[ch] += s_red[ch + off];
-    __syncthreads();
-  }
-  const int64_t s_off = s_red[0];
+  int64_t off = 0;  // global chunk offset of unit u
+  for (int uu = lane; uu < u; uu += 32) off += cv.n_chunks[uu];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+  const float4 q4 = *reinterpret_cast<const float4 *>(qg + (int64_t)row * D + 4 * lane);
+  *reinterpret_cast<float4 *>(&s_q[wr][4 * lane]) = q4;
   const int nch = cv.n_chunks[u];
-  float m = -INFINITY, l = 0.f, a = 0.f;
+  float m = -INFINITY, l = 0.f;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
   if (nch > 0) {
-    const int64_t x0 = s_off, x1 = s_off + nch - 1;
+    const int64_t x0 = off, x1 = off + nch - 1;
     int c0 = (int)(x0 * grid / total_chunks);
     while (c0 + 1 < grid && range_lo(total_chunks, c0 + 1, grid) <= x0) ++c0;
     while (c0 > 0 && range_lo(total_chunks, c0, grid) > x0) --c0;
@@ -212,49 +206,75 @@ __global__ void __launch_bounds__(128) combine_kernel(CacheViewDev cv, const flo
         if (!(rm > -INFINITY)) continue;  // the group saw no chunk of this unit
         const float mn = fmaxf(m, rm);
         const float sa = exp2f(m - mn), sb = exp2f(rm - mn);
-        a = a * sa + rec[4 + ch] * sb;
+        const float4 r4 = *reinterpret_cast<const float4 *>(rec + 4 + 4 * lane);
+        a.x = a.x * sa + r4.x * sb;
+        a.y = a.y * sa + r4.y * sb;
+        a.z = a.z * sa + r4.z * sb;
+        a.w = a.w * sa + r4.w * sb;
         l = l * sa + rl * sb;
         m = mn;
       }
     }
   }
+  __syncwarp();
   // residual rows: exact RoPE(k, pos) . q scores (base-2 logits)
   const int nres = cv.n_res[u];
   if (nres > 0) {
     const int64_t pbase = cv.base_pos[u] + (int64_t)nch * R;
-    if (ch < nres) {
-      const float *kr = cv.k_res + ((int64_t)u * R + ch) * D;
-      const float2 *cs = cv.rope_cs + (pbase + ch - cv.rope_pos0) * NPAIR;
+    for (int tt = lane; tt < nres; tt += 32) {
+      const float *kr = cv.k_res + ((int64_t)u * R + tt) * D;
+      const float2 *cs = cv.rope_cs + (pbase + tt - cv.rope_pos0) * NPAIR;
       float acc = 0.f;
       for (int j = 0; j < NPAIR; ++j) {
         const float2 e = cs[j];
         const float ke = kr[2 * j], ko = kr[2 * j + 1];
-        acc = fmaf(ke * e.x - ko * e.y, s_q[2 * j], acc);
-        acc = fmaf(ke * e.y + ko * e.x, s_q[2 * j + 1], acc);
+        acc = fmaf(ke * e.x - ko * e.y, s_q[wr][2 * j], acc);
+        acc = fmaf(ke * e.y + ko * e.x, s_q[wr][2 * j + 1], acc);
       }
-      s_w[ch] = acc * LOG2E_OVER_SQRTD;
+      s_w[wr][tt] = acc * LOG2E_OVER_SQRTD;
     }
-    __syncthreads();
+    __syncwarp();
     float rm = -INFINITY;
-    for (int tt = 0; tt < nres; ++tt) rm = fmaxf(rm, s_w[tt]);
+    for (int tt = 0; tt < nres; ++tt) rm = fmaxf(rm, s_w[wr][tt]);
     const float mn = fmaxf(m, rm);
     const float sa = (m > -INFINITY) ? exp2f(m - mn) : 0.f;
-    a *= sa;
+    a.x *= sa; a.y *= sa; a.z *= sa; a.w *= sa;
     l *= sa;
     for (int tt = 0; tt < nres; ++tt) {
-      const float p = exp2f(s_w[tt] - mn);
+      const float p = exp2f(s_w[wr][tt] - mn);
+      const float4 v4 = *reinterpret_cast<const float4 *>(cv.v_res + ((int64_t)u * R + tt) * D + 4 * lane);
       l += p;
-      a = fmaf(p, cv.v_res[((int64_t)u * R + tt) * D + ch], a);
+      a.x = fmaf(p, v4.x, a.x);
+      a.y = fmaf(p, v4.y, a.y);
+      a.z = fmaf(p, v4.z, a.z);
+      a.w = fmaf(p, v4.w, a.w);
     }
     m = mn;
   }
-  s_acc[ch] = (l > 0.f) ? a / l : 0.f;
-  __syncthreads();
-  block_fwht128(s_acc);
-  out[(int64_t)row * D + ch] = s_acc[ch];
-  if (lse && ch == 0) lse[row] = (l > 0.f) ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
+  const float inv = (l > 0.f) ? 1.f / l : 0.f;
+  float4 v = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
+  // inverse FWHT in the warp (stages h = 1, 2 in-lane, 4 .. 64 by shuffles)
+  {
+    float p0 = v.x + v.y, p1 = v.x - v.y, p2 = v.z + v.w, p3 = v.z - v.w;
+    v.x = p0 + p2; v.z = p0 - p2; v.y = p1 + p3; v.w = p1 - p3;
+#pragma unroll
+    for (int mm = 1; mm < 32; mm <<= 1) {
+      const float ox = __shfl_xor_sync(0xffffffffu, v.x, mm);
+      const float oy = __shfl_xor_sync(0xffffffffu, v.y, mm);
+      const float oz = __shfl_xor_sync(0xffffffffu, v.z, mm);
+      const float ow = __shfl_xor_sync(0xffffffffu, v.w, mm);
+      if (lane & mm) {
+        v.x = ox - v.x; v.y = oy - v.y; v.z = oz - v.z; v.w = ow - v.w;
+      } else {
+        v.x += ox; v.y += oy; v.z += oz; v.w += ow;
+      }
+    }
+    const float sc = 0.08838834764831845f;
+    v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+  }
+  *reinterpret_cast<float4 *>(out + (int64_t)row * D + 4 * lane) = v;
+  if (lse && lane == 0) lse[row] = (l > 0.f) ? (m + log2f(l)) * 0.6931471805599453f : -INFINITY;
 }
-
 
 }  // namespace nsnkv
 

@@ -663,7 +663,7 @@ static int launch_attend(const CacheViewDev &cv, const float *q, float *out, flo
         <<<grid, AttCfg<G>::THREADS, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
     ++launches;
   }
-  combine_kernel<G, AttCfg<G>::NGRP><<<cv.batch * cv.n_q_heads, 128, 0, st>>>(cv, q, recs, total > 0 ? total : 1,
+  combine_kernel<G, AttCfg<G>::NGRP><<<(cv.batch * cv.n_q_heads + COMBINE_ROWS - 1) / COMBINE_ROWS, 32 * COMBINE_ROWS, 0, st>>>(cv, q, recs, total > 0 ? total : 1,
                                                               grid, out, lse);
   nsnkv_internal_count_launch(launches);
   return nsnkv_internal_check_launch("decode_attend");

@@ -564,7 +564,7 @@ int nsnkv_launch_attend_ws(const CacheViewDev &cv, const float *q, float *out, f
     attend_ws_kernel<G, FOLD, PREC><<<grid, WS_THREADS, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
     ++launches;
   }
-  combine_kernel<G, 2><<<cv.batch * cv.n_q_heads, 128, 0, st>>>(cv, q, recs, total > 0 ? total : 1,
+  combine_kernel<G, 2><<<(cv.batch * cv.n_q_heads + COMBINE_ROWS - 1) / COMBINE_ROWS, 32 * COMBINE_ROWS, 0, st>>>(cv, q, recs, total > 0 ? total : 1,
                                                                 grid, out, lse);
   nsnkv_internal_count_launch(launches);
   return nsnkv_internal_check_launch("decode_attend_ws");
