@@ -164,7 +164,9 @@ __device__ __forceinline__ int k_channel(int t, int kt, int r, int i) {
 // ---------------------------------------------------------------------------
 constexpr int COMBINE_ROWS = 4;  // warps (rows) per CTA
 
-template <int G, int NGRP>
+// ALLREC: every group wrote a record for every unit its CTA touches (m = -inf
+// when it saw none of the unit's chunks), so no ownership test is needed.
+template <int G, int NGRP, bool ALLREC = false>
 __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
     CacheViewDev cv, const float *__restrict__ qg, const float *__restrict__ recs,
     int64_t total_chunks, int grid, float *__restrict__ out, float *__restrict__ lse) {
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
       const int64_t ka = (x0 > clo ? x0 : clo) - clo;
       const int64_t kb = (x1 + 1 < chi ? x1 + 1 : chi) - clo;
       for (int gq = 0; gq < NGRP; ++gq) {
-        if (!(ka + ((gq - ka % NGRP + NGRP) % NGRP) < kb)) continue;
+        if (!ALLREC && !(ka + ((gq - ka % NGRP + NGRP) % NGRP) < kb)) continue;
         const float *rec = record_ptr<G>(const_cast<float *>(recs), (u + c) * NGRP + gq) + h * (4 + D);
         const float rm = rec[0], rl = rec[1];
         if (!(rm > -INFINITY)) continue;  // the group saw no chunk of this unit
@@ -282,3 +284,13 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
 template <int G, bool FOLD, int PREC>
 int nsnkv_launch_attend_ws(const nsnkv::CacheViewDev &cv, const float *q, float *out, float *lse,
                            float *recs, int64_t total, int grid, cudaStream_t st);
+
+// second-generation decode launcher (decode_attend2.cu), G = 1, 2, 4, 8
+template <int G, bool FOLD, int PREC>
+int nsnkv_launch_attend2(const nsnkv::CacheViewDev &cv, const float *q, float *out, float *lse,
+                         float *recs, int64_t total, int grid, cudaStream_t st);
+
+// warp-specialized decode launcher (decode_attend3.cu), G = 1, 2, 4, 8
+template <int G, bool FOLD, int PREC>
+int nsnkv_launch_attend3(const nsnkv::CacheViewDev &cv, const float *q, float *out, float *lse,
+                         float *recs, int64_t total, int grid, cudaStream_t st);

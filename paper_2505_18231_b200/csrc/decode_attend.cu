@@ -614,7 +614,7 @@ static int attend_grid() {
 
 static size_t records_bytes(const CacheViewDev &cv, int G) {
   const int units = cv.batch * cv.n_kv_heads;
-  const int ngrp = G <= 4 ? AttCfg<4>::NGRP : AttCfg<8>::NGRP;
+  const int ngrp = 3;  // max group count over the decode kernels (v1 G<=4, v2)
   return (size_t)(units + attend_grid() + 1) * ngrp * G * (4 + D) * sizeof(float);
 }
 
@@ -627,23 +627,34 @@ extern "C" size_t nsnkv_decode_workspace_bytes(const nsnkv_cache_view *cv_in) {
   return a > b ? a : b;
 }
 
-// NSNKV_DECODE_KERNEL=ws selects the warp-specialized kernel (decode_ws.cu)
-// for G <= 4 -- an explored alternative, ~10 % slower on B200 (its V-warps
-// spend ~20 % of their issue slots waiting for the K-warps' hand-off); the
-// default is the grouped kernel below.
-static bool decode_kernel_grouped() {
+// Kernel selection (NSNKV_DECODE_KERNEL): "v3" (default) the warp-specialized
+// kernel with the shift term on tcgen05 (decode_attend3.cu); "v2" the paired
+// grouped kernel (decode_attend2.cu); "v1" the first-generation grouped
+// kernel below; "ws" the first-generation warp-specialized variant.
+static int decode_kernel_choice() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("NSNKV_DECODE_KERNEL");
-    v = (e && strcmp(e, "ws") == 0) ? 0 : 1;
+    v = (e && strcmp(e, "ws") == 0) ? 0 : (e && strcmp(e, "v1") == 0) ? 1
+      : (e && strcmp(e, "v2") == 0) ? 2 : 3;
   }
-  return v == 1;
+  return v;
 }
 
 template <int G, bool FOLD, int PREC>
 static int launch_attend(const CacheViewDev &cv, const float *q, float *out, float *lse,
                          float *recs, int64_t total, cudaStream_t st) {
-  if (G <= 4 && !decode_kernel_grouped()) {  // warp-specialized kernel (decode_ws.cu)
+  if (decode_kernel_choice() == 3) {
+    int grid = attend_grid();
+    if (total < grid) grid = (int)(total > 0 ? total : 1);
+    return nsnkv_launch_attend3<G, FOLD, PREC>(cv, q, out, lse, recs, total, grid, st);
+  }
+  if (decode_kernel_choice() == 2) {
+    int grid = attend_grid();
+    if (total < grid) grid = (int)(total > 0 ? total : 1);
+    return nsnkv_launch_attend2<G, FOLD, PREC>(cv, q, out, lse, recs, total, grid, st);
+  }
+  if (G <= 4 && decode_kernel_choice() == 0) {  // warp-specialized kernel (decode_ws.cu)
     int grid = attend_grid();
     if (total < grid) grid = (int)(total > 0 ? total : 1);
     return nsnkv_launch_attend_ws<(G <= 4 ? G : 4), FOLD, PREC>(cv, q, out, lse, recs, total,

@@ -1,0 +1,874 @@
+// decode_attend3.cu -- nsnkv_decode_attend, warp-specialized generation:
+// split-K flash-decoding over the packed cache (reference
+// attention.py:83-142 in one pass).
+//
+// Per (unit = batch x kv-head, 64-token chunk), for the G q-heads of the GQA
+// group:
+//   score_t = s1_t * ( s2_t * <HT(q), c_t> + <q, RoPE(o, p0 + tau)> )
+//   out     = FWHT( sum_t softmax_t * s1_t * (s2_t * c'_t + o') )
+//
+// Roles (512 threads, one CTA per SM, stream-K split of the chunk list into
+// work items of CP consecutive chunks of one unit):
+//  * warp 12 (TMA): streams each item's K and V pages into a shared-memory
+//    ring with 1-D bulk copies (cp.async.bulk + mbarrier complete_tx);
+//  * warps 13..15 (item producers, one per consumer group): per item, the
+//    token scales, the value shift vectors and the shift-term B operand
+//    Z[(cos,sin)_j][(chunk, head, hi/lo)] = q . RoPE(o, p0) (split hi + lo
+//    fp16), then ONE thread issues the shift-term product on the 5th-gen
+//    tensor cores:  D[tau][n] = Tab[tau][(cos,sin)_j] . Z  with the constant
+//    Tab = (cos, sin)(tau f_j) resident in TMEM as fp16 hi + lo (16
+//    tcgen05.mma, M = 128 = 2 chunks x 64 positions, N = 16, A from TMEM, B
+//    from shared memory), accumulator in TMEM;
+//  * warps 0..11 (3 consumer groups of 4 warps; warp ws owns token positions
+//    [16 ws, 16 ws + 16) of every chunk): codeword gathers from 64 KB-aligned
+//    shared-memory tables, sign flips, K-side payload products and V-side
+//    value products on mma.sync tensor cores, online softmax; the shift term
+//    arrives by tcgen05.ld straight into the mma accumulator layout.
+// Consumers never synchronise with each other inside a unit: items flow
+// through full / ready / free / empty mbarriers.
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "decode_common.cuh"
+#include "decode_att.cuh"
+#include "tc05.cuh"
+
+namespace nsnkv {
+
+template <int G, bool FOLD, int PREC>
+struct A3 {
+  static constexpr int CP = G <= 4 ? 2 : 1;        // chunks per work item
+  static constexpr int NTP = (2 * G + 7) / 8;      // payload n-tiles: (head, hi/lo) columns
+  static constexpr int NGRP = 3;                   // consumer groups
+  static constexpr int THREADS = 512;
+  static constexpr int PAGE = FOLD ? NSNKV_PAGE_BYTES_2B : NSNKV_PAGE_BYTES_1B;
+  static constexpr int STAGE = CP * 2 * PAGE;
+  static constexpr bool ONE_TABLE = PREC == 2;     // K hi | V hi interleaved per entry
+  static constexpr int TBL = ONE_TABLE ? 65536 : 131072;
+  static constexpr int ZB = 4096;                  // B operand: K 128 x N 16 fp16
+
+  struct Slot {
+    float4 sc[CP][R];  // (s1k*s2k, s1k, s1v*s2v, s1v) per token
+    float ov[CP][D];   // dequantized value shift vectors
+  };
+  struct Prod {        // written by the group's producer warp
+    uint8_t zb[ZB];    // shift-term B operand (canonical no-swizzle K-major)
+    Slot slot[2];
+  };
+  struct Cons {        // consumer-only (group-synchronised at unit changes)
+    union {
+      struct {
+        float acc[G][D];
+        float ml[G][2];
+      } mg;
+      struct {
+        float q[G][D + 4];
+        float qh[G][D];
+      } su;
+    };
+  };
+  struct Bars {
+    uint64_t full[24], empty[24];
+    uint64_t ready[NGRP][2], free_[NGRP][2];
+    uint64_t tabs;
+    uint32_t tmem_base;
+  };
+  static constexpr int BARS = ((int)sizeof(Bars) + 127) / 128 * 128;
+  static constexpr int PROD = ((int)sizeof(Prod) + 127) / 128 * 128;
+  static constexpr int CONS = ((int)sizeof(Cons) + 127) / 128 * 128;
+  // windows: LO = below the 64 KB-aligned tables, HI = above them
+  static constexpr int LO_WIN = MISC_LO_MAX;
+  static constexpr int HI_WIN = ATT_SMEM_BYTES + 1024 - 65536 - TBL;
+  // fast: bars + consumer + producer scratch below, ring above;
+  // precise / balanced: producer scratch above, bars + consumer scratch + ring below
+  static constexpr int RING_WIN = ONE_TABLE ? HI_WIN : LO_WIN - BARS - NGRP * CONS;
+  static constexpr int NSTAGE_RAW = RING_WIN / STAGE;
+  static constexpr int NSTAGE = NSTAGE_RAW > 24 ? 24 : NSTAGE_RAW;
+  static_assert(!ONE_TABLE || BARS + NGRP * (CONS + PROD) <= LO_WIN, "scratch does not fit");
+  static_assert(ONE_TABLE || NGRP * PROD <= HI_WIN, "producer scratch does not fit");
+  static_assert(NSTAGE > NGRP, "ring too shallow");
+  // TMEM columns: Tab hi [0, 64), Tab lo [64, 128), D[g][slot] 16 columns each
+  static constexpr uint32_t TMEM_COLS = 256;
+  static constexpr uint32_t D_COL0 = 128;
+};
+
+// ---------------------------------------------------------------------------
+// Work items: runs of up to CP consecutive chunks of one unit inside the
+// CTA's chunk range [lo, hi).
+struct Item3 {
+  int u, c, end;
+  int64_t x;
+};
+
+__device__ __forceinline__ Item3 item3_seek(int64_t lo, int64_t hi, const int32_t *n_chunks,
+                                            int n_units) {
+  const ChunkCursor cc = cursor_seek(lo, n_chunks, n_units);
+  Item3 it;
+  it.u = cc.u;
+  it.c = cc.c;
+  it.x = lo;
+  const int64_t room = hi - lo;
+  it.end = (int64_t)(cc.n - cc.c) < room ? cc.n : cc.c + (int)room;
+  return it;
+}
+template <int CP>
+__device__ __forceinline__ int item3_count(const Item3 &it) {
+  const int r = it.end - it.c;
+  return r < CP ? r : CP;
+}
+template <int CP>
+__device__ __forceinline__ void item3_next(Item3 &it, int64_t hi, const int32_t *n_chunks,
+                                           int n_units) {
+  const int cnt = item3_count<CP>(it);
+  it.x += cnt;
+  it.c += cnt;
+  if (it.c >= it.end) {
+    if (it.x >= hi) {
+      it.u = n_units;
+      it.c = it.end = 0;
+      return;
+    }
+    int n = 0;
+    while (n == 0 && ++it.u < n_units) n = n_chunks[it.u];
+    it.c = 0;
+    const int64_t room = hi - it.x;
+    it.end = (int64_t)n < room ? n : (int)room;
+  }
+}
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// rtn4_dequant (vq.py:133-136): zero + level * scale, two fp32 roundings
+__device__ __forceinline__ float rtn4(uint32_t level, float zero, float scale) {
+  return __fadd_rn(zero, __fmul_rn((float)level, scale));
+}
+
+template <int G, bool FOLD, int PREC>
+__global__ void __launch_bounds__(512, 1)
+    attend3_kernel(CacheViewDev cv, const float *__restrict__ qg, float *__restrict__ recs,
+                   int64_t total_chunks) {
+  using C = A3<G, FOLD, PREC>;
+  constexpr int CP = C::CP, NTP = C::NTP, NGRP = C::NGRP, NSTAGE = C::NSTAGE;
+  constexpr bool HILO_K = PREC == 0;
+  constexpr bool HILO_V = PREC <= 1;
+  constexpr PageLayout L = page_layout(FOLD ? 2 : 1);
+  constexpr uint32_t PB = (uint32_t)C::PAGE;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_units = cv.batch * cv.n_kv_heads;
+
+  const int grid = gridDim.x;
+  const int64_t lo = range_lo(total_chunks, blockIdx.x, grid);
+  const int64_t hi = range_lo(total_chunks, blockIdx.x + 1, grid);
+  if (lo >= hi) return;
+
+  // ---- shared memory carve-up ----
+  const uint32_t base = smem_u32(smem);
+  const uint32_t tk = (base + 0xffffu) & ~0xffffu;  // tables, 64 KB aligned
+  if (tk - base < (uint32_t)C::BARS) __trap();       // (the window is never 64 KB aligned)
+  uint8_t *lo_win = smem;
+  uint8_t *hi_win = smem + (tk - base) + C::TBL;
+  typename C::Bars &BR = *reinterpret_cast<typename C::Bars *>(lo_win);
+  typename C::Cons *CS = reinterpret_cast<typename C::Cons *>(lo_win + C::BARS);
+  typename C::Prod *PS;
+  uint8_t *ring;
+  if (C::ONE_TABLE) {
+    PS = reinterpret_cast<typename C::Prod *>(lo_win + C::BARS + NGRP * C::CONS);
+    ring = hi_win;
+  } else {
+    PS = reinterpret_cast<typename C::Prod *>(hi_win);
+    ring = lo_win + C::BARS + NGRP * C::CONS;
+  }
+  const uint32_t tab_k = tk;                                  // K table (or K|V interleaved)
+  const uint32_t tab_v = C::ONE_TABLE ? tk + 128u : tk + 0x10000u;
+
+  const Item3 start = item3_seek(lo, hi, cv.n_chunks, n_units);
+  const int first_unit = start.u;
+  const int last_unit = cursor_seek(hi - 1, cv.n_chunks, n_units).u;
+
+  // ---- set-up: barriers, TMEM, tables --------------------------------------
+  if (warp == 12) {
+    tc05::alloc(smem_u32(&BR.tmem_base), C::TMEM_COLS);
+    tc05::relinquish();
+    if (lane == 0) {
+      for (int s = 0; s < NSTAGE; ++s) {
+        mbar_init(&BR.full[s], 1);
+        mbar_init(&BR.empty[s], 5);
+      }
+      for (int q = 0; q < NGRP; ++q)
+        for (int s = 0; s < 2; ++s) {
+          mbar_init(&BR.ready[q][s], 2);
+          mbar_init(&BR.free_[q][s], 4);
+        }
+      mbar_init(&BR.tabs, C::ONE_TABLE ? 128 : 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (!C::ONE_TABLE) {
+        mbar_expect_tx(&BR.tabs, 2 * 65536);
+        tma_load_1d(smem + (tab_k - base), cv.cb_k.tabw, 65536, &BR.tabs);
+        tma_load_1d(smem + (tab_v - base), cv.cb_v.tabw, 65536, &BR.tabs);
+      }
+    }
+  }
+  tc05::fence_before();
+  __syncthreads();
+  tc05::fence_after();
+  const uint32_t tmem = BR.tmem_base;
+
+  if (warp >= 12) {
+    // ======================= producer warpgroup ================================
+    const int pq = warp - 12;  // TMEM lane quarter of this warp
+    if (C::ONE_TABLE) {        // interleave the K and V hi gather tables
+      const int t128 = tid - 384;
+      const uint4 *sk = reinterpret_cast<const uint4 *>(cv.cb_k.tabw);
+      const uint4 *sv = reinterpret_cast<const uint4 *>(cv.cb_v.tabw);
+      uint4 *dst = reinterpret_cast<uint4 *>(smem + (tab_k - base));
+      for (int i = t128; i < NENT * 8; i += 128) {
+        const int e = i >> 3, s = i & 7;
+        dst[e * 16 + s] = sk[e * 16 + s];
+        dst[e * 16 + 8 + s] = sv[e * 16 + s];
+      }
+      mbar_arrive(&BR.tabs);
+    }
+    // constant shift-term A operand into TMEM: lane L <-> position
+    // tau = 16 (L / 32) + L % 16; column j = (cos, sin)(tau f_j) as fp16 hi
+    // (columns 0..63) and lo (64..127)
+    {
+      const int L = 32 * pq + lane;
+      const int tau = 16 * (L >> 5) + (L & 15);
+      const float2 *row = cv.rope_cs + (int64_t)(tau - cv.rope_pos0) * NPAIR;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        uint32_t rh[16], rl[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const float2 cs = row[c0 + c];
+          float ch, cl, sh, sl;
+          split_h(cs.x, ch, cl);
+          split_h(cs.y, sh, sl);
+          rh[c] = pack_h2(ch, sh);
+          rl[c] = pack_h2(cl, sl);
+        }
+        tc05::st_32x32b_x16(tmem + ((uint32_t)(32 * pq) << 16) + c0, rh);
+        tc05::st_32x32b_x16(tmem + ((uint32_t)(32 * pq) << 16) + 64 + c0, rl);
+      }
+      tc05::wait_st();
+      tc05::fence_before();
+    }
+    named_bar(5, 128);  // Tab in TMEM before the first MMA
+    tc05::fence_after();
+
+    if (warp == 12) {
+      // ---------------- TMA: stream the pages of every item ------------------
+      if (lane == 0) {
+        Item3 it = start;
+        for (int k = 0; it.x < hi; ++k) {
+          const int s = k % NSTAGE;
+          if (k >= NSTAGE) mbar_wait(&BR.empty[s], (uint32_t)((k / NSTAGE) - 1) & 1u);
+          const int cnt = item3_count<CP>(it);
+          uint8_t *st = ring + s * C::STAGE;
+          mbar_expect_tx(&BR.full[s], (uint32_t)cnt * 2u * PB);
+          for (int q = 0; q < cnt; ++q) {
+            const int64_t page = cv.page_table[(int64_t)it.u * cv.page_table_stride + it.c + q];
+            tma_load_1d(st + q * 2 * PB, cv.k_pool + page * PB, PB, &BR.full[s]);
+            tma_load_1d(st + q * 2 * PB + PB, cv.v_pool + page * PB, PB, &BR.full[s]);
+          }
+          item3_next<CP>(it, hi, cv.n_chunks, n_units);
+        }
+      }
+    } else {
+      // ---------------- item producer of group gp ------------------------------
+      const int gp = warp - 13;
+      typename C::Prod &P = PS[gp];
+      const uint32_t zb_s = smem_u32(P.zb);
+      Item3 it = start;
+      for (int a = 0; a < gp; ++a) item3_next<CP>(it, hi, cv.n_chunks, n_units);
+      int n = 0;
+      for (int k = gp; it.x < hi; k += NGRP, ++n) {
+        const int cnt = item3_count<CP>(it);
+        const int s = k % NSTAGE, slot = n & 1;
+        // RoPE'd q of the item's unit (read-only path, L1 resident)
+        const int qb = it.u / cv.n_kv_heads, qhk = it.u - qb * cv.n_kv_heads;
+        const float *qs = qg + ((int64_t)qb * cv.n_q_heads + (int64_t)qhk * G) * D;
+        // RoPE rows of the chunks' first positions (global, L2 resident)
+        float2 rcs[CP][2];
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+          const int cc = c < cnt ? c : 0;
+          const int64_t p0 = cv.base_pos[it.u] + (int64_t)(it.c + cc) * R - cv.rope_pos0;
+          rcs[c][0] = cv.rope_cs[p0 * NPAIR + lane];
+          rcs[c][1] = cv.rope_cs[p0 * NPAIR + lane + 32];
+        }
+        if (n >= 2) mbar_wait(&BR.free_[gp][slot], (uint32_t)((n - 2) >> 1) & 1u);
+        mbar_wait(&BR.full[s], (uint32_t)(k / NSTAGE) & 1u);
+        const uint8_t *st = ring + s * C::STAGE;
+        typename C::Slot &SL = P.slot[slot];
+        // token scales (rtn4 s1, f16 s2), keys and values
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int tok = lane + 32 * h2;
+            float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < cnt) {
+              const uint8_t *kp = st + c * 2 * PB, *vp = kp + PB;
+              const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + L.par);
+              const uint16_t *pv = reinterpret_cast<const uint16_t *>(vp + L.par);
+              const uint32_t nk = kp[L.s1n + (tok >> 1)], nv = vp[L.s1n + (tok >> 1)];
+              const float s1k = rtn4((tok & 1) ? (nk >> 4) : (nk & 15u), f16_bits_to_f32(pk[1]),
+                                     f16_bits_to_f32(pk[0]));
+              const float s1v = rtn4((tok & 1) ? (nv >> 4) : (nv & 15u), f16_bits_to_f32(pv[1]),
+                                     f16_bits_to_f32(pv[0]));
+              const float s2k = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(kp + L.s2)[tok]);
+              const float s2v = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + L.s2)[tok]);
+              v4 = make_float4(s1k * s2k, s1k, s1v * s2v, s1v);
+            }
+            SL.sc[c][tok] = v4;
+          }
+          // value shift vector: 4 channels per lane
+          float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (c < cnt) {
+            const uint8_t *vp = st + c * 2 * PB + PB;
+            const uint16_t *pv = reinterpret_cast<const uint16_t *>(vp + L.par);
+            const int gr = lane >> 3;  // channels 4 lane .. +3 are in group (4 lane) / 32
+            const float zs = f16_bits_to_f32(pv[6 + gr]), ss = f16_bits_to_f32(pv[2 + gr]);
+            const uint32_t b2 = *reinterpret_cast<const uint16_t *>(vp + L.on + 2 * lane);
+            o4 = make_float4(rtn4(b2 & 15u, zs, ss), rtn4((b2 >> 4) & 15u, zs, ss),
+                             rtn4((b2 >> 8) & 15u, zs, ss), rtn4((b2 >> 12) & 15u, zs, ss));
+          }
+          *reinterpret_cast<float4 *>(&SL.ov[c][4 * lane]) = o4;
+        }
+        // the previous item's MMA has consumed Zb
+        if (n >= 1) mbar_wait(&BR.ready[gp][slot ^ 1], (uint32_t)((n - 1) >> 1) & 1u);
+        // Z[(cos,sin)_j][n]: lane handles pairs j = lane, lane + 32 of every chunk
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int j = lane + 32 * jj;
+            float he = 0.f, ho = 0.f;
+            if (c < cnt) {
+              const uint8_t *kp = st + c * 2 * PB;
+              const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + L.par);
+              const int gr = j >> 4;
+              const uint32_t b = kp[L.on + j];
+              const float osc = f16_bits_to_f32(pk[2 + gr]), oz = f16_bits_to_f32(pk[6 + gr]);
+              const float oe = rtn4(b & 15u, oz, osc), oo = rtn4(b >> 4, oz, osc);
+              const float2 cs = rcs[c][jj];
+              he = oe * cs.x - oo * cs.y;  // RoPE(o, p0)
+              ho = oe * cs.y + oo * cs.x;
+            }
+            // canonical layout offset of (n, k = 2j): kt = j/8, kh = (j%8)/4, k0 = 2 (j%4)
+            const uint32_t kofs = (uint32_t)((j >> 3) * 512 + ((j >> 2) & 1) * 128 + (j & 3) * 4);
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+              const float2 qv = __ldg(reinterpret_cast<const float2 *>(qs + h * D + 2 * j));
+              const float al = qv.x * he + qv.y * ho;
+              const float be = qv.y * he - qv.x * ho;
+              float ah, alo, bh, blo;
+              split_h(al, ah, alo);
+              split_h(be, bh, blo);
+              // column n = 8c + 2h + part (CP = 2) or 2h + part (CP = 1)
+              const int nn = CP == 2 ? 8 * c + 2 * h : 2 * h;
+              const uint32_t o0 = kofs + (uint32_t)((nn >> 3) * 256 + (nn & 7) * 16);
+              const uint32_t o1 = kofs + (uint32_t)(((nn + 1) >> 3) * 256 + ((nn + 1) & 7) * 16);
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + o0), "r"(pack_h2(ah, bh)));
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + o1), "r"(pack_h2(alo, blo)));
+            }
+            if (CP == 2 && G < 4) {  // unused head columns of this chunk: zero
+#pragma unroll
+              for (int h = G; h < 4; ++h) {
+                const int nn = 8 * c + 2 * h;
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + kofs + (uint32_t)((nn >> 3) * 256 + (nn & 7) * 16)), "r"(0u));
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + kofs + (uint32_t)((nn >> 3) * 256 + ((nn + 1) & 7) * 16)), "r"(0u));
+              }
+            }
+          }
+        }
+        tc05::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&BR.ready[gp][slot]);  // scales and value shift vectors
+          mbar_arrive(&BR.empty[s]);         // this warp is done with the stage
+          tc05::fence_after();
+          const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (2 * gp + slot));
+          constexpr uint32_t idesc = tc05::idesc_f16(128, 16);
+#pragma unroll
+          for (int kt = 0; kt < 8; ++kt)
+            tc05::mma_f16_ts(dcol, tmem + 8 * kt, tc05::smem_desc(zb_s + 512 * kt, 128, 256), idesc,
+                             kt > 0);
+#pragma unroll
+          for (int kt = 0; kt < 8; ++kt)
+            tc05::mma_f16_ts(dcol, tmem + 64 + 8 * kt, tc05::smem_desc(zb_s + 512 * kt, 128, 256),
+                             idesc, 1);
+          tc05::commit(smem_u32(&BR.ready[gp][slot]));
+        }
+        __syncwarp();
+        for (int a = 0; a < NGRP; ++a) item3_next<CP>(it, hi, cv.n_chunks, n_units);
+      }
+    }
+  } else {
+    // ======================= consumer groups ===================================
+    const int g = lane >> 2, t = lane & 3;
+    const int grp = warp >> 2;
+    const int ws = warp & 3;
+    const int ci = 32 * ws + lane;
+    const int bar_id = 1 + grp;
+    typename C::Cons &S = CS[grp];
+    typename C::Prod &P = PS[grp];
+
+    const uint32_t slot16 = (uint32_t)((lane & 7) * 16);
+    const uint32_t lbk = (tab_k & 0xffff0000u) | (tab_k & 0xffu) | slot16;
+    const uint32_t lbv = (tab_v & 0xffff0000u) | (tab_v & 0xffu) | slot16;
+    constexpr uint32_t LO_OFS = C::ONE_TABLE ? 0u : 128u;  // hi -> lo half of an entry
+    const uint32_t vsel0 = 0x7604u | ((uint32_t)(2 * (g & 1)) << 4);
+    const uint32_t vsel1 = 0x7604u | ((uint32_t)(2 * (g & 1) + 1) << 4);
+    const uint32_t psel = (g & 1) ? 0x7632u : 0x5410u;
+
+    uint32_t qB[NTP][8][2];
+    float accV[NTP][8][4];
+    float m_run[NTP], l_run[NTP];
+
+    auto write_empty = [&](int unit) {
+      if (ws == 0 && lane < G) {
+        float *rec = record_ptr<G>(recs, (unit + blockIdx.x) * NGRP + grp);
+        rec[lane * (4 + D)] = -INFINITY;
+      }
+    };
+
+    // merge the 4 warps' partials in a fixed order (3, 2, 1, 0) through one
+    // [G][D] buffer; warp 0 writes the record
+    auto flush_unit = [&](int unit) {
+      float lw[NTP];
+#pragma unroll
+      for (int nt = 0; nt < NTP; ++nt) {
+        float l = l_run[nt];
+        l += __shfl_xor_sync(0xffffffffu, l, 4);
+        l += __shfl_xor_sync(0xffffffffu, l, 8);
+        l += __shfl_xor_sync(0xffffffffu, l, 16);
+        lw[nt] = l;
+      }
+      named_bar(bar_id, 128);
+      for (int r = 3; r >= 0; --r) {
+        if (ws == r) {
+          float mnew[NTP], lnew[NTP];
+#pragma unroll
+          for (int nt = 0; nt < NTP; ++nt) {
+            const int h = 4 * nt + t;
+            mnew[nt] = -INFINITY;
+            lnew[nt] = 0.f;
+            if (h >= G) continue;
+            float sa = 1.f, sb = 0.f, m = m_run[nt], l = lw[nt];
+            if (r < 3) {
+              const float mb = S.mg.ml[h][0], lb = S.mg.ml[h][1];
+              const float mx = fmaxf(m, mb);
+              sa = mx > -INFINITY ? exp2f(m - mx) : 0.f;
+              sb = mx > -INFINITY ? exp2f(mb - mx) : 0.f;
+              l = l * sa + lb * sb;
+              m = mx;
+            }
+            if (r > 0) {
+#pragma unroll
+              for (int mt = 0; mt < 8; ++mt) {
+                const int c = 16 * g + 8 * (mt >> 2) + 2 * (mt & 3);
+                float a0 = (accV[nt][mt][0] + accV[nt][mt][1]) * sa;
+                float a1 = (accV[nt][mt][2] + accV[nt][mt][3]) * sa;
+                if (r < 3) {
+                  a0 = fmaf(S.mg.acc[h][c], sb, a0);
+                  a1 = fmaf(S.mg.acc[h][c + 1], sb, a1);
+                }
+                S.mg.acc[h][c] = a0;
+                S.mg.acc[h][c + 1] = a1;
+              }
+              mnew[nt] = m;
+              lnew[nt] = l;
+            } else {
+              float *rec = record_ptr<G>(recs, (unit + blockIdx.x) * NGRP + grp) + h * (4 + D);
+#pragma unroll
+              for (int mt = 0; mt < 8; ++mt) {
+                const int c = 16 * g + 8 * (mt >> 2) + 2 * (mt & 3);
+                const float a0 = fmaf(S.mg.acc[h][c], sb, (accV[nt][mt][0] + accV[nt][mt][1]) * sa);
+                const float a1 = fmaf(S.mg.acc[h][c + 1], sb, (accV[nt][mt][2] + accV[nt][mt][3]) * sa);
+                *reinterpret_cast<float2 *>(rec + 4 + c) = make_float2(a0, a1);
+              }
+              if (g == 0) {
+                rec[0] = m;
+                rec[1] = l;
+              }
+            }
+          }
+          if (r > 0) {
+            __syncwarp();  // every lane read ml before it is overwritten
+#pragma unroll
+            for (int nt = 0; nt < NTP; ++nt) {
+              const int h = 4 * nt + t;
+              if (h < G && g == 0) {
+                S.mg.ml[h][0] = mnew[nt];
+                S.mg.ml[h][1] = lnew[nt];
+              }
+            }
+          }
+        }
+        named_bar(bar_id, 128);
+      }
+    };
+
+    auto setup_unit = [&](int unit) {
+      const int b = unit / cv.n_kv_heads, hk = unit - b * cv.n_kv_heads;
+      const float *qs = qg + ((int64_t)b * cv.n_q_heads + (int64_t)hk * G) * D;
+      for (int i = ci; i < G * D; i += 128) S.su.q[i / D][i % D] = qs[i];
+      named_bar(bar_id, 128);
+      for (int h = ws; h < G; h += 4) {  // HT(q), 4 values per lane
+        float4 v = *reinterpret_cast<float4 *>(&S.su.q[h][4 * lane]);
+        float a = v.x + v.y, bq = v.x - v.y, c = v.z + v.w, d = v.z - v.w;
+        v.x = a + c; v.z = a - c; v.y = bq + d; v.w = bq - d;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+          const float ox = __shfl_xor_sync(0xffffffffu, v.x, m);
+          const float oy = __shfl_xor_sync(0xffffffffu, v.y, m);
+          const float oz = __shfl_xor_sync(0xffffffffu, v.z, m);
+          const float ow = __shfl_xor_sync(0xffffffffu, v.w, m);
+          if (lane & m) {
+            v.x = ox - v.x; v.y = oy - v.y; v.z = oz - v.z; v.w = ow - v.w;
+          } else {
+            v.x += ox; v.y += oy; v.z += oz; v.w += ow;
+          }
+        }
+        const float sc = 0.08838834764831845f;
+        v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+        *reinterpret_cast<float4 *>(&S.su.qh[h][4 * lane]) = v;
+      }
+      named_bar(bar_id, 128);
+#pragma unroll
+      for (int nt = 0; nt < NTP; ++nt) {
+        const int h = 4 * nt + (g >> 1);
+#pragma unroll
+        for (int kt = 0; kt < 8; ++kt) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            float v0 = 0.f, v1 = 0.f;
+            if (h < G) {
+              float h0, l0, h1, l1;
+              split_h(S.su.qh[h][k_channel(t, kt, r, 0)], h0, l0);
+              split_h(S.su.qh[h][k_channel(t, kt, r, 1)], h1, l1);
+              v0 = (g & 1) ? l0 : h0;
+              v1 = (g & 1) ? l1 : h1;
+            }
+            qB[nt][kt][r] = pack_h2(v0, v1);
+          }
+        }
+        m_run[nt] = -INFINITY;
+        l_run[nt] = 0.f;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) accV[nt][mt][r] = 0.f;
+      }
+      named_bar(bar_id, 128);  // the set-up buffer aliases the merge buffer
+    };
+
+    Item3 cur = start;
+    for (int a = 0; a < grp; ++a) item3_next<CP>(cur, hi, cv.n_chunks, n_units);
+    int cur_unit = -1;
+    int mark_next = first_unit;
+    int n = 0;
+    mbar_wait(&BR.tabs, 0);
+
+    for (int k = grp; cur.x < hi; k += NGRP, ++n) {
+      if (cur.u != cur_unit) {
+        if (cur_unit >= 0) {
+          flush_unit(cur_unit);
+          mark_next = cur_unit + 1;
+        }
+        for (int u = mark_next; u < cur.u; ++u) write_empty(u);
+        mark_next = cur.u;
+        setup_unit(cur.u);
+        cur_unit = cur.u;
+      }
+      const int cnt = item3_count<CP>(cur);
+      const int s = k % NSTAGE, slot = n & 1;
+      mbar_wait(&BR.full[s], (uint32_t)(k / NSTAGE) & 1u);
+      const uint8_t *st = ring + s * C::STAGE;
+
+      // ---- K side: payload dot products on tensor cores ----------------------
+      const int tok0 = 16 * ws + g, tok1 = tok0 + 8;
+      float pd[CP][NTP][2];
+#pragma unroll
+      for (int c = 0; c < CP; ++c) {
+#pragma unroll
+        for (int nt = 0; nt < NTP; ++nt) pd[c][nt][0] = pd[c][nt][1] = 0.f;
+        if (c < cnt) {
+          const uint32_t kpa = smem_u32(st + c * 2 * PB);
+          const uint32_t ik0 = lds32(kpa + L.idx + tok0 * NSUB + 4 * t);
+          const uint32_t ik1 = lds32(kpa + L.idx + tok1 * NSUB + 4 * t);
+          uint32_t sk0 = 0, sk1 = 0;
+          if (FOLD) {
+            sk0 = lds32(kpa + (FOLD ? L.sgn : 0) + tok0 * 16 + 4 * t);
+            sk1 = lds32(kpa + (FOLD ? L.sgn : 0) + tok1 * 16 + 4 * t);
+          }
+          float d1[NTP][2][4];
+#pragma unroll
+          for (int nt = 0; nt < NTP; ++nt)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) d1[nt][0][r] = d1[nt][1][r] = 0.f;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const uint32_t sel = 0x7604u | ((uint32_t)m << 4);
+            const uint32_t a0 = prmt(ik0, lbk, sel), a1 = prmt(ik1, lbk, sel);
+            uint4 h0 = lds128(a0), h1 = lds128(a1);
+            uint4 l0 = make_uint4(0, 0, 0, 0), l1 = l0;
+            if (HILO_K) {
+              l0 = lds128(a0 + LO_OFS);
+              l1 = lds128(a1 + LO_OFS);
+            }
+            if (FOLD) {
+              uint32_t *ph0 = &h0.x, *ph1 = &h1.x, *pl0 = &l0.x, *pl1 = &l1.x;
+#pragma unroll
+              for (int p = 0; p < 4; ++p) {
+                const uint32_t w0 = sk0 << (15 - 4 * m - p);
+                const uint32_t w1 = sk1 << (15 - 4 * m - p);
+                ph0[p] = xor_sign(ph0[p], w0);
+                ph1[p] = xor_sign(ph1[p], w1);
+                if (HILO_K) {
+                  pl0[p] = xor_sign(pl0[p], w0);
+                  pl1[p] = xor_sign(pl1[p], w1);
+                }
+              }
+            }
+#pragma unroll
+            for (int nt = 0; nt < NTP; ++nt) {
+              mma16816(d1[nt][0], h0.x, h1.x, h0.y, h1.y, qB[nt][2 * m][0], qB[nt][2 * m][1]);
+              mma16816(d1[nt][1], h0.z, h1.z, h0.w, h1.w, qB[nt][2 * m + 1][0], qB[nt][2 * m + 1][1]);
+              if (HILO_K) {
+                mma16816(d1[nt][0], l0.x, l1.x, l0.y, l1.y, qB[nt][2 * m][0], qB[nt][2 * m][1]);
+                mma16816(d1[nt][1], l0.z, l1.z, l0.w, l1.w, qB[nt][2 * m + 1][0],
+                         qB[nt][2 * m + 1][1]);
+              }
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < NTP; ++nt) {
+            pd[c][nt][0] = (d1[nt][0][0] + d1[nt][1][0]) + (d1[nt][0][1] + d1[nt][1][1]);
+            pd[c][nt][1] = (d1[nt][0][2] + d1[nt][1][2]) + (d1[nt][0][3] + d1[nt][1][3]);
+          }
+        }
+      }
+
+      // ---- shift term (tensor memory) and token scales from the producer -----
+      mbar_wait(&BR.ready[grp][slot], (uint32_t)(n >> 1) & 1u);
+      tc05::fence_after();
+      const typename C::Slot &SL = P.slot[slot];
+      float sh[CP][NTP][2];
+      {
+        const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (2 * grp + slot));
+        float r4[CP][NTP][4];
+#pragma unroll
+        for (int c = 0; c < CP; ++c)
+#pragma unroll
+          for (int nt = 0; nt < NTP; ++nt)
+            // lanes 32 ws + 16 c (+g, +8+g); columns (chunk c | head group nt) x 8
+            tc05::ld_16x256b(tmem + ((uint32_t)(32 * ws + 16 * c) << 16) +
+                                 (dcol - tmem) + (uint32_t)(8 * (CP == 2 ? c : nt)),
+                             r4[c][nt]);
+        tc05::wait_ld();
+#pragma unroll
+        for (int c = 0; c < CP; ++c)
+#pragma unroll
+          for (int nt = 0; nt < NTP; ++nt) {
+            sh[c][nt][0] = r4[c][nt][0] + r4[c][nt][1];
+            sh[c][nt][1] = r4[c][nt][2] + r4[c][nt][3];
+          }
+      }
+      float4 sct[CP][2];
+#pragma unroll
+      for (int c = 0; c < CP; ++c) {
+        sct[c][0] = SL.sc[c][tok0];
+        sct[c][1] = SL.sc[c][tok1];
+      }
+
+      // ---- scores and online softmax (base 2) -------------------------------
+      uint32_t pf[CP][NTP][2];
+      float wsum[CP][NTP];
+#pragma unroll
+      for (int nt = 0; nt < NTP; ++nt) {
+        const int h = 4 * nt + t;
+        float x[CP][2];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < CP; ++c)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            x[c][r] = (sct[c][r].x * pd[c][nt][r] + sct[c][r].y * sh[c][nt][r]) * LOG2E_OVER_SQRTD;
+            if (c < cnt) mx = fmaxf(mx, x[c][r]);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        const float m_new = fmaxf(m_run[nt], mx);
+        if (m_new > m_run[nt]) {
+          const float rr = exp2f(m_run[nt] - m_new);
+          l_run[nt] *= rr;
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) accV[nt][mt][q] *= rr;
+          m_run[nt] = m_new;
+        }
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+          float p0 = exp2f(x[c][0] - m_new), p1 = exp2f(x[c][1] - m_new);
+          if (h >= G || c >= cnt) p0 = p1 = 0.f;
+          l_run[nt] += p0 + p1;
+          float ws2 = p0 * sct[c][0].w + p1 * sct[c][1].w;
+          ws2 += __shfl_xor_sync(0xffffffffu, ws2, 4);
+          ws2 += __shfl_xor_sync(0xffffffffu, ws2, 8);
+          ws2 += __shfl_xor_sync(0xffffffffu, ws2, 16);
+          wsum[c][nt] = ws2;
+          float h0, l0, h1, l1;
+          split_h(p0 * sct[c][0].z, h0, l0);
+          split_h(p1 * sct[c][1].z, h1, l1);
+          const uint32_t X0 = pack_h2(h0, l0);
+          const uint32_t X1 = pack_h2(h1, l1);
+          const int hs = g >> 1;
+          const int srcA = 8 * t + hs, srcB = 8 * t + 4 + hs;
+          const uint32_t y0a = __shfl_sync(0xffffffffu, X0, srcA);
+          const uint32_t y0b = __shfl_sync(0xffffffffu, X0, srcB);
+          const uint32_t y1a = __shfl_sync(0xffffffffu, X1, srcA);
+          const uint32_t y1b = __shfl_sync(0xffffffffu, X1, srcB);
+          pf[c][nt][0] = prmt(y0a, y0b, psel);
+          pf[c][nt][1] = prmt(y1a, y1b, psel);
+        }
+      }
+
+      // ---- V side: accumulate P' . codewords on tensor cores -----------------
+      const int vt0 = 16 * ws + 2 * t;
+#pragma unroll
+      for (int c = 0; c < CP; ++c) {
+        if (c >= cnt) break;
+        const uint32_t vpa = smem_u32(st + c * 2 * PB + PB);
+        uint32_t iv[4], sv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int tok = vt0 + (q & 1) + ((q & 2) ? 8 : 0);
+          iv[q] = lds32(vpa + L.idx + tok * NSUB + 4 * (g >> 1));
+          sv[q] = FOLD ? (lds32(vpa + (FOLD ? L.sgn : 0) + tok * 16 + 4 * (g >> 1)) >> (8 * (g & 1))) : 0u;
+        }
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg) {
+          const uint32_t sel = sg ? vsel1 : vsel0;
+          uint4 yh[4], yl[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t a = prmt(iv[q], lbv, sel);
+            yh[q] = lds128(a);
+            yl[q] = HILO_V ? lds128(a + LO_OFS) : make_uint4(0, 0, 0, 0);
+            if (FOLD) {
+              uint32_t *ph = &yh[q].x, *pl = &yl[q].x;
+#pragma unroll
+              for (int p = 0; p < 4; ++p) {
+                const uint32_t wk = sv[q] << (15 - 4 * sg - p);
+                ph[p] = xor_sign(ph[p], wk);
+                if (HILO_V) pl[p] = xor_sign(pl[p], wk);
+              }
+            }
+          }
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int mt = 4 * sg + p;
+            const uint32_t *h0p = &yh[0].x, *h1p = &yh[1].x, *h2p = &yh[2].x, *h3p = &yh[3].x;
+            const uint32_t a0h = prmt(h0p[p], h1p[p], 0x5410u), a1h = prmt(h0p[p], h1p[p], 0x7632u);
+            const uint32_t a2h = prmt(h2p[p], h3p[p], 0x5410u), a3h = prmt(h2p[p], h3p[p], 0x7632u);
+#pragma unroll
+            for (int nt = 0; nt < NTP; ++nt)
+              mma16816(accV[nt][mt], a0h, a1h, a2h, a3h, pf[c][nt][0], pf[c][nt][1]);
+            if (HILO_V) {
+              const uint32_t *l0p = &yl[0].x, *l1p = &yl[1].x, *l2p = &yl[2].x, *l3p = &yl[3].x;
+              const uint32_t a0l = prmt(l0p[p], l1p[p], 0x5410u), a1l = prmt(l0p[p], l1p[p], 0x7632u);
+              const uint32_t a2l = prmt(l2p[p], l3p[p], 0x5410u), a3l = prmt(l2p[p], l3p[p], 0x7632u);
+#pragma unroll
+              for (int nt = 0; nt < NTP; ++nt)
+                mma16816(accV[nt][mt], a0l, a1l, a2l, a3l, pf[c][nt][0], pf[c][nt][1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 o4 = *reinterpret_cast<const float4 *>(&SL.ov[c][16 * g + 4 * q4]);
+          const int mt0 = 4 * (q4 >> 1) + 2 * (q4 & 1);
+#pragma unroll
+          for (int nt = 0; nt < NTP; ++nt) {
+            accV[nt][mt0][0] = fmaf(wsum[c][nt], o4.x, accV[nt][mt0][0]);
+            accV[nt][mt0][2] = fmaf(wsum[c][nt], o4.y, accV[nt][mt0][2]);
+            accV[nt][mt0 + 1][0] = fmaf(wsum[c][nt], o4.z, accV[nt][mt0 + 1][0]);
+            accV[nt][mt0 + 1][2] = fmaf(wsum[c][nt], o4.w, accV[nt][mt0 + 1][2]);
+          }
+        }
+      }
+      // release the stage and the producer slot (scales, value shifts, TMEM D)
+      tc05::fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&BR.empty[s]);
+        mbar_arrive(&BR.free_[grp][slot]);
+      }
+      for (int a = 0; a < NGRP; ++a) item3_next<CP>(cur, hi, cv.n_chunks, n_units);
+    }
+    if (cur_unit >= 0) {
+      flush_unit(cur_unit);
+      mark_next = cur_unit + 1;
+    }
+    for (int u = mark_next; u <= last_unit; ++u) write_empty(u);
+  }
+
+  tc05::fence_before();
+  __syncthreads();
+  if (warp == 12) {
+    tc05::fence_after();
+    tc05::dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+}  // namespace nsnkv
+
+using namespace nsnkv;
+
+template <int G, bool FOLD, int PREC>
+int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, float *lse,
+                         float *recs, int64_t total, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attend3_kernel<G, FOLD, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         ATT_SMEM_BYTES);
+    attr = true;
+  }
+  int launches = 0;
+  if (total > 0) {
+    attend3_kernel<G, FOLD, PREC><<<grid, 512, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
+    ++launches;
+  }
+  combine_kernel<G, 3, true>
+      <<<(cv.batch * cv.n_q_heads + COMBINE_ROWS - 1) / COMBINE_ROWS, 32 * COMBINE_ROWS, 0, st>>>(
+          cv, q, recs, total > 0 ? total : 1, grid, out, lse);
+  ++launches;
+  nsnkv_internal_count_launch(launches);
+  return nsnkv_internal_check_launch("decode_attend");
+}
+
+#define NSNKV_A3_INST(GG, FF, PP)                                                            \
+  template int nsnkv_launch_attend3<GG, FF, PP>(const CacheViewDev &, const float *, float *, \
+                                                float *, float *, int64_t, int, cudaStream_t);
+#define NSNKV_A3_INST_G(GG) \
+  NSNKV_A3_INST(GG, true, 0) NSNKV_A3_INST(GG, true, 1) NSNKV_A3_INST(GG, true, 2) \
+  NSNKV_A3_INST(GG, false, 0) NSNKV_A3_INST(GG, false, 1) NSNKV_A3_INST(GG, false, 2)
+NSNKV_A3_INST_G(1)
+NSNKV_A3_INST_G(2)
+NSNKV_A3_INST_G(4)
+NSNKV_A3_INST_G(8)
