@@ -16,7 +16,7 @@ from pathlib import Path
 from .errors import raise_for_status
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libnsnkv_b200.so"
+LIB_PATH = Path(os.environ["NSNKV_LIB"]) if os.environ.get("NSNKV_LIB") else _PKG / "libnsnkv_b200.so"
 
 
 def _load() -> ctypes.CDLL:

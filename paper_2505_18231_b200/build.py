@@ -44,11 +44,17 @@ def needs_rebuild() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_rebuild():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """trace=True builds libnsnkv_b200_trace.so with -DNSNKV_TRACE (a debug
+    timeline of CTA 0 in the decode kernel, scripts/trace_decode.py)."""
+    lib = LIB.with_name("libnsnkv_b200_trace.so") if trace else LIB
+    extra = os.environ.get("NSNKV_EXTRA_FLAGS", "").split()
+    if extra:
+        lib = lib.with_name(os.environ.get("NSNKV_LIB_NAME", lib.name))
+    if not force and not trace and not needs_rebuild():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"),
-           *[str(CSRC / s) for s in SOURCES], "-o", str(LIB) + ".tmp", "-lcudart"]
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DNSNKV_TRACE"] if trace else []), *extra, "-I", str(ROOT / "include"),
+           *[str(CSRC / s) for s in SOURCES], "-o", str(lib) + ".tmp", "-lcudart"]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -57,10 +63,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("nvcc failed building libnsnkv_b200.so")
     if verbose and (res.stdout or res.stderr):
         sys.stderr.write(res.stdout + res.stderr)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

@@ -20,6 +20,8 @@ single-head facade in ``api.py`` is a 1 x 1 batch.
 
 from __future__ import annotations
 
+import os
+
 import enum
 import math
 import struct
@@ -143,8 +145,10 @@ class PagedKvCache:
     def __init__(self, config: CacheConfig, batch: int, n_kv_heads: int, max_tokens: int = 0,
                  cb_k: Codebook | None = None, cb_v: Codebook | None = None,
                  base_position: int = 0, device=None, check_finite: bool = True,
-                 precision: str = "precise"):
+                 precision: str | None = None):
         config.check_gpu_path()
+        if precision is None:  # deployment default; NSNKV_PRECISION overrides
+            precision = os.environ.get("NSNKV_PRECISION", "precise")
         self.check_finite = check_finite
         # decode codeword precision: "precise" = fp16 hi + lo
         # on both sides, "balanced" = plain fp16 scores / hi + lo values,

@@ -16,9 +16,9 @@
 //    Z[(cos,sin)_j][(chunk, head, hi/lo)] = q . RoPE(o, p0) (split hi + lo
 //    fp16), then ONE thread issues the shift-term product on the 5th-gen
 //    tensor cores:  D[tau][n] = Tab[tau][(cos,sin)_j] . Z  with the constant
-//    Tab = (cos, sin)(tau f_j) resident in TMEM as fp16 hi + lo (16
-//    tcgen05.mma, M = 128 = 2 chunks x 64 positions, N = 16, A from TMEM, B
-//    from shared memory), accumulator in TMEM;
+//    Tab = (cos, sin)(tau f_j) resident in TMEM as fp16 hi + lo stacked along
+//    M (8 tcgen05.mma, M = 128 = 64 positions x hi/lo, N = 16 = 2 chunks x 4
+//    heads x Z hi/lo, A from TMEM, B from shared memory), accumulator in TMEM;
 //  * warps 0..11 (3 consumer groups of 4 warps; warp ws owns token positions
 //    [16 ws, 16 ws + 16) of every chunk): codeword gathers from 64 KB-aligned
 //    shared-memory tables, sign flips, K-side payload products and V-side
@@ -36,6 +36,24 @@
 
 namespace nsnkv {
 
+#ifdef NSNKV_TRACE
+// debug timeline of CTA 0 (built only into the trace library): per warp,
+// 4096 records of clock64 << 24 | event << 16 | item, plain stores
+__device__ unsigned long long g_trace[16][4096];
+#define A3_TRACE(role, ev, item)                                                          \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && tr_i < 4096u)                      \
+      g_trace[threadIdx.x >> 5][tr_i++] =                                                \
+          ((unsigned long long)clock64() << 24) | ((unsigned long long)(ev) << 16) | (unsigned)(item); \
+  } while (0)
+#define A3_TRACE_DECL unsigned tr_i = 0
+#else
+#define A3_TRACE(role, ev, item) \
+  do {                           \
+  } while (0)
+#define A3_TRACE_DECL
+#endif
+
 template <int G, bool FOLD, int PREC>
 struct A3 {
   static constexpr int CP = G <= 4 ? 2 : 1;        // chunks per work item
@@ -43,18 +61,29 @@ struct A3 {
   static constexpr int NGRP = 3;                   // consumer groups
   static constexpr int THREADS = 512;
   static constexpr int PAGE = FOLD ? NSNKV_PAGE_BYTES_2B : NSNKV_PAGE_BYTES_1B;
-  static constexpr int STAGE = CP * 2 * PAGE;
+  // pages split in two streams: the payload (idx [+ signs]) for the consumer
+  // groups, the 256-byte tail (s2, s1 / o nibbles, RTN-4 params) for the
+  // producers, each with its own ring so producers can run ahead
+  static constexpr int MAIN = FOLD ? 2048 : 1024;
+  static constexpr int META = 256;
+  static constexpr int STAGE = CP * 2 * MAIN;
+  static constexpr int TAILS = CP * 2 * META;  // producer's staged page tails per item
   static constexpr bool ONE_TABLE = PREC == 2;     // K hi | V hi interleaved per entry
   static constexpr int TBL = ONE_TABLE ? 65536 : 131072;
-  static constexpr int ZB = 4096;                  // B operand: K 128 x N 16 fp16
+  static constexpr int ZB = 4096 * (ONE_TABLE ? 2 : 1);  // B operand: K 128 x N fp16
+  static constexpr int NSLOT = ONE_TABLE ? 4 : 2;  // producer -> consumer item slots
+  static constexpr int NZB = 1;                    // shift-term B operand buffers per group
+  static constexpr int BATCH = ONE_TABLE ? 2 : 1;  // items per shift-term MMA chain
+  static constexpr int NB = 16 * BATCH;            // MMA N: (item, chunk, head, Z hi/lo)
 
   struct Slot {
     float4 sc[CP][R];  // (s1k*s2k, s1k, s1v*s2v, s1v) per token
     float ov[CP][D];   // dequantized value shift vectors
   };
   struct Prod {        // written by the group's producer warp
-    uint8_t zb[ZB];    // shift-term B operand (canonical no-swizzle K-major)
-    Slot slot[2];
+    uint8_t zb[NZB][ZB];  // shift-term B operand (canonical no-swizzle MN-major)
+    uint8_t tails[TAILS]; // page tails of the item being produced (K c0, V c0, K c1, V c1)
+    Slot slot[NSLOT];
   };
   struct Cons {        // consumer-only (group-synchronised at unit changes)
     union {
@@ -70,7 +99,7 @@ struct A3 {
   };
   struct Bars {
     uint64_t full[24], empty[24];
-    uint64_t ready[NGRP][2], free_[NGRP][2];
+    uint64_t ready[NGRP][NSLOT], free_[NGRP][NSLOT];
     uint64_t tabs;
     uint32_t tmem_base;
   };
@@ -80,17 +109,22 @@ struct A3 {
   // windows: LO = below the 64 KB-aligned tables, HI = above them
   static constexpr int LO_WIN = MISC_LO_MAX;
   static constexpr int HI_WIN = ATT_SMEM_BYTES + 1024 - 65536 - TBL;
-  // fast: bars + consumer + producer scratch below, ring above;
-  // precise / balanced: producer scratch above, bars + consumer scratch + ring below
-  static constexpr int RING_WIN = ONE_TABLE ? HI_WIN : LO_WIN - BARS - NGRP * CONS;
+  // fast: bars, consumer scratch and as many producer scratch blocks as fit
+  // below, the other producer blocks and the ring above; precise / balanced:
+  // producer scratch above, bars + consumer scratch + ring below
+  static constexpr int PLO_RAW = (LO_WIN - BARS - NGRP * CONS) / PROD;
+  static constexpr int PLO = ONE_TABLE ? (PLO_RAW > NGRP ? NGRP : PLO_RAW) : 0;
+  static constexpr int RING_WIN =
+      ONE_TABLE ? HI_WIN - (NGRP - PLO) * PROD : LO_WIN - BARS - NGRP * CONS;
   static constexpr int NSTAGE_RAW = RING_WIN / STAGE;
-  static constexpr int NSTAGE = NSTAGE_RAW > 24 ? 24 : NSTAGE_RAW;
-  static_assert(!ONE_TABLE || BARS + NGRP * (CONS + PROD) <= LO_WIN, "scratch does not fit");
+  static constexpr int NS = (NSTAGE_RAW > 24 ? 24 : NSTAGE_RAW) / NGRP;  // stages per group
+  static constexpr int NSTAGE = NS * NGRP;
+  static_assert(!ONE_TABLE || BARS + NGRP * CONS <= LO_WIN, "scratch does not fit");
   static_assert(ONE_TABLE || NGRP * PROD <= HI_WIN, "producer scratch does not fit");
-  static_assert(NSTAGE > NGRP, "ring too shallow");
-  // TMEM columns: Tab hi [0, 64), Tab lo [64, 128), D[g][slot] 16 columns each
-  static constexpr uint32_t TMEM_COLS = 256;
-  static constexpr uint32_t D_COL0 = 128;
+  static_assert(NS >= 2, "ring too shallow");
+  // TMEM columns: Tab (hi | lo stacked in lanes) [0, 64), D[g][slot] 16 columns each
+  static constexpr uint32_t D_COL0 = 64;
+  static constexpr uint32_t TMEM_COLS = D_COL0 + 16 * NGRP * NSLOT <= 256 ? 256 : 512;
 };
 
 // ---------------------------------------------------------------------------
@@ -147,6 +181,39 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// producer-side wait: back off with nanosleep so a waiting producer does not
+// take issue slots from the consumer warps of its SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  while (!ok) {
+    __nanosleep(64);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
 // rtn4_dequant (vq.py:133-136): zero + level * scale, two fp32 roundings
 __device__ __forceinline__ float rtn4(uint32_t level, float zero, float scale) {
   return __fadd_rn(zero, __fmul_rn((float)level, scale));
@@ -165,6 +232,7 @@ __global__ void __launch_bounds__(512, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_units = cv.batch * cv.n_kv_heads;
+  A3_TRACE_DECL;
 
   const int grid = gridDim.x;
   const int64_t lo = range_lo(total_chunks, blockIdx.x, grid);
@@ -179,15 +247,14 @@ __global__ void __launch_bounds__(512, 1)
   uint8_t *hi_win = smem + (tk - base) + C::TBL;
   typename C::Bars &BR = *reinterpret_cast<typename C::Bars *>(lo_win);
   typename C::Cons *CS = reinterpret_cast<typename C::Cons *>(lo_win + C::BARS);
-  typename C::Prod *PS;
-  uint8_t *ring;
-  if (C::ONE_TABLE) {
-    PS = reinterpret_cast<typename C::Prod *>(lo_win + C::BARS + NGRP * C::CONS);
-    ring = hi_win;
-  } else {
-    PS = reinterpret_cast<typename C::Prod *>(hi_win);
-    ring = lo_win + C::BARS + NGRP * C::CONS;
-  }
+  // producer scratch of group g
+  auto prod_of = [&](int g) -> typename C::Prod & {
+    uint8_t *p = g < C::PLO ? lo_win + C::BARS + NGRP * C::CONS + g * C::PROD
+                            : hi_win + (g - C::PLO) * C::PROD;
+    return *reinterpret_cast<typename C::Prod *>(p);
+  };
+  uint8_t *ring = C::ONE_TABLE ? hi_win + (NGRP - C::PLO) * C::PROD
+                               : lo_win + C::BARS + NGRP * C::CONS;
   const uint32_t tab_k = tk;                                  // K table (or K|V interleaved)
   const uint32_t tab_v = C::ONE_TABLE ? tk + 128u : tk + 0x10000u;
 
@@ -201,12 +268,12 @@ __global__ void __launch_bounds__(512, 1)
     tc05::relinquish();
     if (lane == 0) {
       for (int s = 0; s < NSTAGE; ++s) {
-        mbar_init(&BR.full[s], 1);
-        mbar_init(&BR.empty[s], 5);
+        mbar_init(&BR.full[s], 32);  // the streaming warp's lanes (cp.async arrivals)
+        mbar_init(&BR.empty[s], 4);  // the group's 4 consumer warps
       }
       for (int q = 0; q < NGRP; ++q)
-        for (int s = 0; s < 2; ++s) {
-          mbar_init(&BR.ready[q][s], 2);
+        for (int s = 0; s < C::NSLOT; ++s) {
+          mbar_init(&BR.ready[q][s], 2);  // the group's producer + the MMA commit
           mbar_init(&BR.free_[q][s], 4);
         }
       mbar_init(&BR.tabs, C::ONE_TABLE ? 128 : 1);
@@ -238,27 +305,26 @@ __global__ void __launch_bounds__(512, 1)
       }
       mbar_arrive(&BR.tabs);
     }
-    // constant shift-term A operand into TMEM: lane L <-> position
-    // tau = 16 (L / 32) + L % 16; column j = (cos, sin)(tau f_j) as fp16 hi
-    // (columns 0..63) and lo (64..127)
+    // constant shift-term A operand into TMEM, fp16 hi and lo parts stacked
+    // along M: lane L = 32 q + 16 p + i holds position tau = 16 q + i, part p
+    // (0 = hi, 1 = lo); column j = (cos, sin)(tau f_j)
     {
       const int L = 32 * pq + lane;
       const int tau = 16 * (L >> 5) + (L & 15);
+      const bool lo_part = (L >> 4) & 1;
       const float2 *row = cv.rope_cs + (int64_t)(tau - cv.rope_pos0) * NPAIR;
 #pragma unroll 1
       for (int c0 = 0; c0 < 64; c0 += 16) {
-        uint32_t rh[16], rl[16];
+        uint32_t rv[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           const float2 cs = row[c0 + c];
           float ch, cl, sh, sl;
           split_h(cs.x, ch, cl);
           split_h(cs.y, sh, sl);
-          rh[c] = pack_h2(ch, sh);
-          rl[c] = pack_h2(cl, sl);
+          rv[c] = lo_part ? pack_h2(cl, sl) : pack_h2(ch, sh);
         }
-        tc05::st_32x32b_x16(tmem + ((uint32_t)(32 * pq) << 16) + c0, rh);
-        tc05::st_32x32b_x16(tmem + ((uint32_t)(32 * pq) << 16) + 64 + c0, rl);
+        tc05::st_32x32b_x16(tmem + ((uint32_t)(32 * pq) << 16) + c0, rv);
       }
       tc05::wait_st();
       tc05::fence_before();
@@ -266,153 +332,284 @@ __global__ void __launch_bounds__(512, 1)
     named_bar(5, 128);  // Tab in TMEM before the first MMA
     tc05::fence_after();
 
+    constexpr int NSLOT = C::NSLOT, NZB = C::NZB;
     if (warp == 12) {
-      // ---------------- TMA: stream the pages of every item ------------------
-      if (lane == 0) {
-        Item3 it = start;
-        for (int k = 0; it.x < hi; ++k) {
-          const int s = k % NSTAGE;
-          if (k >= NSTAGE) mbar_wait(&BR.empty[s], (uint32_t)((k / NSTAGE) - 1) & 1u);
-          const int cnt = item3_count<CP>(it);
-          uint8_t *st = ring + s * C::STAGE;
-          mbar_expect_tx(&BR.full[s], (uint32_t)cnt * 2u * PB);
-          for (int q = 0; q < cnt; ++q) {
-            const int64_t page = cv.page_table[(int64_t)it.u * cv.page_table_stride + it.c + q];
-            tma_load_1d(st + q * 2 * PB, cv.k_pool + page * PB, PB, &BR.full[s]);
-            tma_load_1d(st + q * 2 * PB + PB, cv.v_pool + page * PB, PB, &BR.full[s]);
+      // ---------------- warp 12: page streaming --------------------------------
+      // payload (idx [+ signs]) of every item into its group's ring (NS stages
+      // per group: no head-of-line blocking between groups) with 16-byte
+      // cp.async from all 32 lanes; every lane's completion arrives on the
+      // stage's full barrier (cp.async.mbarrier.arrive.noinc, 32 arrivals).
+      // Page ids come from 32-entry windows of the page table (per group).
+      {
+        constexpr uint32_t MB = (uint32_t)C::MAIN;
+        constexpr int V16 = C::MAIN / 16 / 32;  // 16-byte vectors per lane per page
+        constexpr int NS = C::NS;
+        int wu[NGRP], wc0[NGRP], nis[NGRP];
+        int32_t wv[NGRP];
+        Item3 tc[NGRP];
+        {
+          Item3 x = start;
+#pragma unroll
+          for (int g = 0; g < NGRP; ++g) {
+            tc[g] = x;
+            item3_next<CP>(x, hi, cv.n_chunks, n_units);
+            wu[g] = -1, wc0[g] = 0, wv[g] = 0, nis[g] = 0;
           }
-          item3_next<CP>(it, hi, cv.n_chunks, n_units);
+        }
+        for (;;) {
+          bool any = false, progress = false;
+#pragma unroll
+          for (int g = 0; g < NGRP; ++g) {
+            if (tc[g].x >= hi) continue;
+            any = true;
+            const int n = nis[g], s2 = g * NS + n % NS;
+            bool ok = n < NS;
+            if (!ok) ok = __shfl_sync(0xffffffffu, lane == 0 ? (int)mbar_test(&BR.empty[s2], (uint32_t)((n / NS) - 1) & 1u) : 0, 0);
+            if (!ok) continue;
+            const Item3 &it2 = tc[g];
+            const int cnt2 = item3_count<CP>(it2);
+            int64_t pg[CP];
+#pragma unroll
+            for (int q = 0; q < CP; ++q) {
+              const int c = it2.c + (q < cnt2 ? q : 0);
+              if (it2.u != wu[g] || c < wc0[g] || c >= wc0[g] + 32) {
+                wu[g] = it2.u;
+                wc0[g] = c;
+                const int cc = c + lane;
+                wv[g] = cc < it2.end ? cv.page_table[(int64_t)it2.u * cv.page_table_stride + cc] : 0;
+              }
+              pg[q] = (int64_t)__shfl_sync(0xffffffffu, wv[g], c - wc0[g]);
+            }
+            const uint32_t st2 = smem_u32(ring + s2 * C::STAGE);
+#pragma unroll
+            for (int q = 0; q < CP; ++q) {
+              if (q < cnt2) {
+                const uint8_t *ks = cv.k_pool + pg[q] * PB, *vs = cv.v_pool + pg[q] * PB;
+#pragma unroll
+                for (int v = 0; v < V16; ++v) {
+                  const uint32_t o = (uint32_t)(16 * (lane + 32 * v));
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + o),
+                               "l"(ks + o)
+                               : "memory");
+                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + MB + o),
+                               "l"(vs + o)
+                               : "memory");
+                }
+              }
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&BR.full[s2]))
+                         : "memory");
+            A3_TRACE(12, 0, 3 * n + g);
+            for (int a = 0; a < NGRP; ++a) item3_next<CP>(tc[g], hi, cv.n_chunks, n_units);
+            ++nis[g];
+            progress = true;
+          }
+          if (!any) break;
+          if (!progress) __nanosleep(256);
         }
       }
     } else {
       // ---------------- item producer of group gp ------------------------------
       const int gp = warp - 13;
-      typename C::Prod &P = PS[gp];
-      const uint32_t zb_s = smem_u32(P.zb);
+      typename C::Prod &P = prod_of(gp);
+      constexpr int HPR = CP == 2 ? G : 8;  // heads per Z row pair (CP = 1: two 4-head rows)
       Item3 it = start;
       for (int a = 0; a < gp; ++a) item3_next<CP>(it, hi, cv.n_chunks, n_units);
+      int cur_unit = -1;
+      float2 qz[2][HPR];  // q pairs (2j, 2j+1) of this lane's j = lane, lane + 32
+      // RoPE rows of the chunks' first positions, prefetched one item ahead
+      auto rope_rows = [&](const Item3 &x, float2 (&r)[CP][2]) {
+        if (x.x >= hi) return;
+        const int cnt = item3_count<CP>(x);
+        const int64_t pb = cv.base_pos[x.u] - cv.rope_pos0;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+          const int64_t p0 = pb + (int64_t)(x.c + (c < cnt ? c : 0)) * R;
+          r[c][0] = __ldg(cv.rope_cs + p0 * NPAIR + lane);
+          r[c][1] = __ldg(cv.rope_cs + p0 * NPAIR + lane + 32);
+        }
+      };
+      float2 rcs[CP][2];
+      rope_rows(it, rcs);
+      // page tails (last 256 bytes of the K and V page of each chunk), two
+      // items ahead: lane l loads 32 bytes of tail l / 8 (K c0, V c0, K c1, V c1)
+      auto tail_load = [&](const Item3 &x, uint4 (&r)[2]) {
+        r[0] = r[1] = make_uint4(0, 0, 0, 0);
+        if (x.x >= hi) return;
+        const int t = lane >> 3, c = t >> 1;
+        if (c >= item3_count<CP>(x)) return;
+        const int64_t page = cv.page_table[(int64_t)x.u * cv.page_table_stride + x.c + c];
+        const uint8_t *src = ((t & 1) ? cv.v_pool : cv.k_pool) + page * PB + C::MAIN + 32 * (lane & 7);
+        r[0] = __ldg(reinterpret_cast<const uint4 *>(src));
+        r[1] = __ldg(reinterpret_cast<const uint4 *>(src + 16));
+      };
+      Item3 it1 = it;
+      for (int a = 0; a < NGRP; ++a) item3_next<CP>(it1, hi, cv.n_chunks, n_units);
+      uint4 tl0[2], tl1[2];  // tails of items n and n + 1
+      tail_load(it, tl0);
+      tail_load(it1, tl1);
       int n = 0;
       for (int k = gp; it.x < hi; k += NGRP, ++n) {
         const int cnt = item3_count<CP>(it);
-        const int s = k % NSTAGE, slot = n & 1;
-        // RoPE'd q of the item's unit (read-only path, L1 resident)
-        const int qb = it.u / cv.n_kv_heads, qhk = it.u - qb * cv.n_kv_heads;
-        const float *qs = qg + ((int64_t)qb * cv.n_q_heads + (int64_t)qhk * G) * D;
-        // RoPE rows of the chunks' first positions (global, L2 resident)
-        float2 rcs[CP][2];
+        const int s = k % NSTAGE, slot = n % NSLOT;
+        if (it.u != cur_unit) {
+          cur_unit = it.u;
+          const int qb = it.u / cv.n_kv_heads, qhk = it.u - qb * cv.n_kv_heads;
+          const float *qs = qg + ((int64_t)qb * cv.n_q_heads + (int64_t)qhk * G) * D;
 #pragma unroll
-        for (int c = 0; c < CP; ++c) {
-          const int cc = c < cnt ? c : 0;
-          const int64_t p0 = cv.base_pos[it.u] + (int64_t)(it.c + cc) * R - cv.rope_pos0;
-          rcs[c][0] = cv.rope_cs[p0 * NPAIR + lane];
-          rcs[c][1] = cv.rope_cs[p0 * NPAIR + lane + 32];
+          for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int h = 0; h < HPR; ++h)
+              qz[jj][h] = h < G ? __ldg(reinterpret_cast<const float2 *>(qs + h * D + 2 * (lane + 32 * jj)))
+                                : make_float2(0.f, 0.f);
         }
-        if (n >= 2) mbar_wait(&BR.free_[gp][slot], (uint32_t)((n - 2) >> 1) & 1u);
-        mbar_wait(&BR.full[s], (uint32_t)(k / NSTAGE) & 1u);
-        const uint8_t *st = ring + s * C::STAGE;
+        Item3 nx = it1;  // next item of this producer: prefetch its RoPE rows
+        float2 rcs_next[CP][2];
+        rope_rows(nx, rcs_next);
+        Item3 it2 = it1;  // two items ahead: prefetch its page tails
+        for (int a = 0; a < NGRP; ++a) item3_next<CP>(it2, hi, cv.n_chunks, n_units);
+        uint4 tl2[2];
+        tail_load(it2, tl2);
+        A3_TRACE(warp, 0, n);
+        if (n >= NSLOT) mbar_wait_sleep(&BR.free_[gp][slot], (uint32_t)((n / NSLOT) - 1) & 1u);
+        A3_TRACE(warp, 1, n);
+        // stage the item's page tails; field offsets are relative to the tail
+        __syncwarp();
+        *reinterpret_cast<uint4 *>(P.tails + 32 * lane) = tl0[0];
+        *reinterpret_cast<uint4 *>(P.tails + 32 * lane + 16) = tl0[1];
+        __syncwarp();
+        A3_TRACE(warp, 2, n);
+        const uint8_t *st = P.tails - C::MAIN;
+        constexpr uint32_t TP = 2u * C::META;  // chunk stride in the staged tails
         typename C::Slot &SL = P.slot[slot];
-        // token scales (rtn4 s1, f16 s2), keys and values
+        // token scales (rtn4 s1, f16 s2) of tokens 2 lane, 2 lane + 1, keys and values
 #pragma unroll
         for (int c = 0; c < CP; ++c) {
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int tok = lane + 32 * h2;
-            float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (c < cnt) {
-              const uint8_t *kp = st + c * 2 * PB, *vp = kp + PB;
-              const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + L.par);
-              const uint16_t *pv = reinterpret_cast<const uint16_t *>(vp + L.par);
-              const uint32_t nk = kp[L.s1n + (tok >> 1)], nv = vp[L.s1n + (tok >> 1)];
-              const float s1k = rtn4((tok & 1) ? (nk >> 4) : (nk & 15u), f16_bits_to_f32(pk[1]),
-                                     f16_bits_to_f32(pk[0]));
-              const float s1v = rtn4((tok & 1) ? (nv >> 4) : (nv & 15u), f16_bits_to_f32(pv[1]),
-                                     f16_bits_to_f32(pv[0]));
-              const float s2k = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(kp + L.s2)[tok]);
-              const float s2v = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + L.s2)[tok]);
-              v4 = make_float4(s1k * s2k, s1k, s1v * s2v, s1v);
-            }
-            SL.sc[c][tok] = v4;
-          }
-          // value shift vector: 4 channels per lane
-          float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+          float4 o4 = v0;
           if (c < cnt) {
-            const uint8_t *vp = st + c * 2 * PB + PB;
-            const uint16_t *pv = reinterpret_cast<const uint16_t *>(vp + L.par);
-            const int gr = lane >> 3;  // channels 4 lane .. +3 are in group (4 lane) / 32
-            const float zs = f16_bits_to_f32(pv[6 + gr]), ss = f16_bits_to_f32(pv[2 + gr]);
+            const uint8_t *kp = st + c * TP, *vp = kp + C::META;
+            const uint32_t pk01 = *reinterpret_cast<const uint32_t *>(kp + L.par);  // s1 scale, zero
+            const uint32_t pv01 = *reinterpret_cast<const uint32_t *>(vp + L.par);
+            const uint32_t nk = kp[L.s1n + lane], nv = vp[L.s1n + lane];
+            const uint32_t s2k = *reinterpret_cast<const uint32_t *>(kp + L.s2 + 4 * lane);
+            const uint32_t s2v = *reinterpret_cast<const uint32_t *>(vp + L.s2 + 4 * lane);
+            const float ksc = f16_bits_to_f32(pk01 & 0xffffu), kz = f16_bits_to_f32(pk01 >> 16);
+            const float vsc = f16_bits_to_f32(pv01 & 0xffffu), vz = f16_bits_to_f32(pv01 >> 16);
+            const float s1k0 = rtn4(nk & 15u, kz, ksc), s1k1 = rtn4(nk >> 4, kz, ksc);
+            const float s1v0 = rtn4(nv & 15u, vz, vsc), s1v1 = rtn4(nv >> 4, vz, vsc);
+            const float k20 = f16_bits_to_f32(s2k & 0xffffu), k21 = f16_bits_to_f32(s2k >> 16);
+            const float v20 = f16_bits_to_f32(s2v & 0xffffu), v21 = f16_bits_to_f32(s2v >> 16);
+            v0 = make_float4(s1k0 * k20, s1k0, s1v0 * v20, s1v0);
+            v1 = make_float4(s1k1 * k21, s1k1, s1v1 * v21, s1v1);
+            // value shift vector: channels 4 lane .. 4 lane + 3 (group lane / 8)
+            const int gr = lane >> 3;
+            const float zs = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + L.par)[6 + gr]);
+            const float ss = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + L.par)[2 + gr]);
             const uint32_t b2 = *reinterpret_cast<const uint16_t *>(vp + L.on + 2 * lane);
             o4 = make_float4(rtn4(b2 & 15u, zs, ss), rtn4((b2 >> 4) & 15u, zs, ss),
                              rtn4((b2 >> 8) & 15u, zs, ss), rtn4((b2 >> 12) & 15u, zs, ss));
           }
+          SL.sc[c][2 * lane] = v0;
+          SL.sc[c][2 * lane + 1] = v1;
           *reinterpret_cast<float4 *>(&SL.ov[c][4 * lane]) = o4;
         }
-        // the previous item's MMA has consumed Zb
-        if (n >= 1) mbar_wait(&BR.ready[gp][slot ^ 1], (uint32_t)((n - 1) >> 1) & 1u);
-        // Z[(cos,sin)_j][n]: lane handles pairs j = lane, lane + 32 of every chunk
+        A3_TRACE(warp, 3, n);
+        // the MMA chain that last used this Z buffer (batch m - NZB) is done
+        constexpr int BATCH = C::BATCH, NB = C::NB;
+        const int m = n / BATCH, e = n % BATCH;
+        if (m >= NZB) {
+          const int n0 = (m - NZB) * BATCH;
+          mbar_wait_sleep(&BR.ready[gp][n0 % NSLOT], (uint32_t)((n0 / NSLOT) & 1));
+        }
+        A3_TRACE(warp, 4, n);
+        const uint32_t zb_s = smem_u32(P.zb[m % NZB]);
+        // Z (MN-major B operand): element (k, n) at (k/8)*256 + (n/8)*128 +
+        // (k%8)*16 + (n%8)*2 with k = 2j (cos coefficient a_j) / 2j + 1 (sin
+        // coefficient b_j) and n = 8 (chunk | head group) + 2 head + (hi | lo):
+        // each (j, chunk) writes two 16-byte rows (a_j and b_j for 4 heads x hi/lo);
+        // lanes 4..7 of every 8 store the b row first (conflict-free phases)
 #pragma unroll
         for (int c = 0; c < CP; ++c) {
+          float osc = 0.f, oz = 0.f, osc2 = 0.f, oz2 = 0.f;
+          uint32_t ob0 = 0, ob1 = 0;
+          if (c < cnt) {
+            const uint8_t *kp = st + c * TP;
+            const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + L.par);
+            osc = f16_bits_to_f32(pk[2 + (lane >> 4)]);      // group of channels 2 lane
+            oz = f16_bits_to_f32(pk[6 + (lane >> 4)]);
+            osc2 = f16_bits_to_f32(pk[2 + 2 + (lane >> 4)]); // channels 2 (lane + 32)
+            oz2 = f16_bits_to_f32(pk[6 + 2 + (lane >> 4)]);
+            ob0 = kp[L.on + lane];
+            ob1 = kp[L.on + lane + 32];
+          }
 #pragma unroll
           for (int jj = 0; jj < 2; ++jj) {
             const int j = lane + 32 * jj;
-            float he = 0.f, ho = 0.f;
-            if (c < cnt) {
-              const uint8_t *kp = st + c * 2 * PB;
-              const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + L.par);
-              const int gr = j >> 4;
-              const uint32_t b = kp[L.on + j];
-              const float osc = f16_bits_to_f32(pk[2 + gr]), oz = f16_bits_to_f32(pk[6 + gr]);
-              const float oe = rtn4(b & 15u, oz, osc), oo = rtn4(b >> 4, oz, osc);
-              const float2 cs = rcs[c][jj];
-              he = oe * cs.x - oo * cs.y;  // RoPE(o, p0)
-              ho = oe * cs.y + oo * cs.x;
-            }
-            // canonical layout offset of (n, k = 2j): kt = j/8, kh = (j%8)/4, k0 = 2 (j%4)
-            const uint32_t kofs = (uint32_t)((j >> 3) * 512 + ((j >> 2) & 1) * 128 + (j & 3) * 4);
+            const uint32_t b = jj ? ob1 : ob0;
+            const float sc_ = jj ? osc2 : osc, z_ = jj ? oz2 : oz;
+            const float oe = rtn4(b & 15u, z_, sc_), oo = rtn4(b >> 4, z_, sc_);
+            const float2 cs = rcs[c][jj];
+            const float he = c < cnt ? oe * cs.x - oo * cs.y : 0.f;  // RoPE(o, p0)
+            const float ho = c < cnt ? oe * cs.y + oo * cs.x : 0.f;
 #pragma unroll
-            for (int h = 0; h < G; ++h) {
-              const float2 qv = __ldg(reinterpret_cast<const float2 *>(qs + h * D + 2 * j));
-              const float al = qv.x * he + qv.y * ho;
-              const float be = qv.y * he - qv.x * ho;
-              float ah, alo, bh, blo;
-              split_h(al, ah, alo);
-              split_h(be, bh, blo);
-              // column n = 8c + 2h + part (CP = 2) or 2h + part (CP = 1)
-              const int nn = CP == 2 ? 8 * c + 2 * h : 2 * h;
-              const uint32_t o0 = kofs + (uint32_t)((nn >> 3) * 256 + (nn & 7) * 16);
-              const uint32_t o1 = kofs + (uint32_t)(((nn + 1) >> 3) * 256 + ((nn + 1) & 7) * 16);
-              asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + o0), "r"(pack_h2(ah, bh)));
-              asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + o1), "r"(pack_h2(alo, blo)));
-            }
-            if (CP == 2 && G < 4) {  // unused head columns of this chunk: zero
+            for (int hg = 0; hg < (HPR + 3) / 4; ++hg) {
+              uint32_t ra[4], rb[4];
 #pragma unroll
-              for (int h = G; h < 4; ++h) {
-                const int nn = 8 * c + 2 * h;
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + kofs + (uint32_t)((nn >> 3) * 256 + (nn & 7) * 16)), "r"(0u));
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(zb_s + kofs + (uint32_t)((nn >> 3) * 256 + ((nn + 1) & 7) * 16)), "r"(0u));
+              for (int hh = 0; hh < 4; ++hh) {
+                const int h = 4 * hg + hh;
+                float al = 0.f, be = 0.f;
+                if (h < HPR) {
+                  const float2 qv = qz[jj][h < HPR ? h : 0];
+                  al = qv.x * he + qv.y * ho;
+                  be = qv.y * he - qv.x * ho;
+                }
+                // hi = fp16 (al, be), lo = fp16 of the remainders
+                const __half2 hh2 = __floats2half2_rn(al, be);
+                const float2 hf = __half22float2(hh2);
+                const __half2 lh2 = __floats2half2_rn(al - hf.x, be - hf.y);
+                const uint32_t hw = *reinterpret_cast<const uint32_t *>(&hh2);
+                const uint32_t lw = *reinterpret_cast<const uint32_t *>(&lh2);
+                ra[hh] = prmt(hw, lw, 0x5410u);  // (a hi, a lo)
+                rb[hh] = prmt(hw, lw, 0x7632u);  // (b hi, b lo)
               }
+              const int n1 = (CP == 2 ? c : hg) + 2 * e;
+              const uint32_t row = zb_s + (uint32_t)((j >> 2) * (NB * 16) + n1 * 128 + (j & 3) * 32);
+              const bool bfirst = (lane >> 2) & 1;
+              const uint32_t a0 = bfirst ? row + 16 : row, a1 = bfirst ? row : row + 16;
+              const uint4 v0 = bfirst ? make_uint4(rb[0], rb[1], rb[2], rb[3]) : make_uint4(ra[0], ra[1], ra[2], ra[3]);
+              const uint4 v1 = bfirst ? make_uint4(ra[0], ra[1], ra[2], ra[3]) : make_uint4(rb[0], rb[1], rb[2], rb[3]);
+              asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a0), "r"(v0.x), "r"(v0.y), "r"(v0.z), "r"(v0.w));
+              asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a1), "r"(v1.x), "r"(v1.y), "r"(v1.z), "r"(v1.w));
             }
           }
         }
         tc05::fence_proxy_async();
         __syncwarp();
+        A3_TRACE(warp, 5, n);
         if (lane == 0) {
           mbar_arrive(&BR.ready[gp][slot]);  // scales and value shift vectors
-          mbar_arrive(&BR.empty[s]);         // this warp is done with the stage
-          tc05::fence_after();
-          const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (2 * gp + slot));
-          constexpr uint32_t idesc = tc05::idesc_f16(128, 16);
+          if (e == BATCH - 1 || nx.x >= hi) {  // issue the batch's shift-term MMA chain
+            tc05::fence_after();
+            const int nf = m * BATCH;          // first item of the batch
+            const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (NSLOT * gp + nf % NSLOT));
+            constexpr uint32_t idesc = tc05::idesc_f16(128, NB) | (1u << 16);  // B MN-major
 #pragma unroll
-          for (int kt = 0; kt < 8; ++kt)
-            tc05::mma_f16_ts(dcol, tmem + 8 * kt, tc05::smem_desc(zb_s + 512 * kt, 128, 256), idesc,
-                             kt > 0);
-#pragma unroll
-          for (int kt = 0; kt < 8; ++kt)
-            tc05::mma_f16_ts(dcol, tmem + 64 + 8 * kt, tc05::smem_desc(zb_s + 512 * kt, 128, 256),
-                             idesc, 1);
-          tc05::commit(smem_u32(&BR.ready[gp][slot]));
+            for (int kt = 0; kt < 8; ++kt)
+              tc05::mma_f16_ts(dcol, tmem + 8 * kt,
+                               tc05::smem_desc(zb_s + (uint32_t)(kt * NB * 32), NB * 16, 128), idesc,
+                               kt > 0);
+            for (int q = nf; q <= n; ++q) tc05::commit(smem_u32(&BR.ready[gp][q % NSLOT]));
+          }
         }
         __syncwarp();
-        for (int a = 0; a < NGRP; ++a) item3_next<CP>(it, hi, cv.n_chunks, n_units);
+        A3_TRACE(warp, 6, n);
+        it = nx;
+        it1 = it2;
+        tl0[0] = tl1[0], tl0[1] = tl1[1];
+        tl1[0] = tl2[0], tl1[1] = tl2[1];
+#pragma unroll
+        for (int c = 0; c < CP; ++c) rcs[c][0] = rcs_next[c][0], rcs[c][1] = rcs_next[c][1];
       }
     }
   } else {
@@ -423,7 +620,7 @@ __global__ void __launch_bounds__(512, 1)
     const int ci = 32 * ws + lane;
     const int bar_id = 1 + grp;
     typename C::Cons &S = CS[grp];
-    typename C::Prod &P = PS[grp];
+    typename C::Prod &P = prod_of(grp);
 
     const uint32_t slot16 = (uint32_t)((lane & 7) * 16);
     const uint32_t lbk = (tab_k & 0xffff0000u) | (tab_k & 0xffu) | slot16;
@@ -594,8 +791,10 @@ __global__ void __launch_bounds__(512, 1)
         cur_unit = cur.u;
       }
       const int cnt = item3_count<CP>(cur);
-      const int s = k % NSTAGE, slot = n & 1;
-      mbar_wait(&BR.full[s], (uint32_t)(k / NSTAGE) & 1u);
+      const int s = grp * C::NS + n % C::NS, slot = n % C::NSLOT;
+      A3_TRACE(warp, 0, n);
+      mbar_wait(&BR.full[s], (uint32_t)(n / C::NS) & 1u);
+      A3_TRACE(warp, 1, n);
       const uint8_t *st = ring + s * C::STAGE;
 
       // ---- K side: payload dot products on tensor cores ----------------------
@@ -606,7 +805,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int nt = 0; nt < NTP; ++nt) pd[c][nt][0] = pd[c][nt][1] = 0.f;
         if (c < cnt) {
-          const uint32_t kpa = smem_u32(st + c * 2 * PB);
+          const uint32_t kpa = smem_u32(st + c * 2 * C::MAIN);
           const uint32_t ik0 = lds32(kpa + L.idx + tok0 * NSUB + 4 * t);
           const uint32_t ik1 = lds32(kpa + L.idx + tok1 * NSUB + 4 * t);
           uint32_t sk0 = 0, sk1 = 0;
@@ -663,28 +862,35 @@ __global__ void __launch_bounds__(512, 1)
       }
 
       // ---- shift term (tensor memory) and token scales from the producer -----
-      mbar_wait(&BR.ready[grp][slot], (uint32_t)(n >> 1) & 1u);
+      A3_TRACE(warp, 2, n);
+#ifndef NSNKV_TRACE_NOREADY
+      mbar_wait(&BR.ready[grp][slot], (uint32_t)(n / C::NSLOT) & 1u);
+#endif
+      A3_TRACE(warp, 3, n);
       tc05::fence_after();
       const typename C::Slot &SL = P.slot[slot];
       float sh[CP][NTP][2];
       {
-        const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (2 * grp + slot));
-        float r4[CP][NTP][4];
+        const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (C::NSLOT * grp + slot));
+        float r4[CP][NTP][2][4];
 #pragma unroll
         for (int c = 0; c < CP; ++c)
 #pragma unroll
           for (int nt = 0; nt < NTP; ++nt)
-            // lanes 32 ws + 16 c (+g, +8+g); columns (chunk c | head group nt) x 8
-            tc05::ld_16x256b(tmem + ((uint32_t)(32 * ws + 16 * c) << 16) +
-                                 (dcol - tmem) + (uint32_t)(8 * (CP == 2 ? c : nt)),
-                             r4[c][nt]);
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+              // lanes 32 ws + 16 p (+g, +8+g): Tab hi / lo rows of the slice;
+              // columns (chunk c | head group nt) x 8: (head, Z hi / lo)
+              tc05::ld_16x256b(tmem + ((uint32_t)(32 * ws + 16 * p) << 16) +
+                                   (dcol - tmem) + (uint32_t)(8 * (CP == 2 ? c : nt)),
+                               r4[c][nt][p]);
         tc05::wait_ld();
 #pragma unroll
         for (int c = 0; c < CP; ++c)
 #pragma unroll
           for (int nt = 0; nt < NTP; ++nt) {
-            sh[c][nt][0] = r4[c][nt][0] + r4[c][nt][1];
-            sh[c][nt][1] = r4[c][nt][2] + r4[c][nt][3];
+            sh[c][nt][0] = (r4[c][nt][0][0] + r4[c][nt][0][1]) + (r4[c][nt][1][0] + r4[c][nt][1][1]);
+            sh[c][nt][1] = (r4[c][nt][0][2] + r4[c][nt][0][3]) + (r4[c][nt][1][2] + r4[c][nt][1][3]);
           }
       }
       float4 sct[CP][2];
@@ -753,7 +959,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
       for (int c = 0; c < CP; ++c) {
         if (c >= cnt) break;
-        const uint32_t vpa = smem_u32(st + c * 2 * PB + PB);
+        const uint32_t vpa = smem_u32(st + c * 2 * C::MAIN + C::MAIN);
         uint32_t iv[4], sv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -813,6 +1019,7 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
       // release the stage and the producer slot (scales, value shifts, TMEM D)
+      A3_TRACE(warp, 4, n);
       tc05::fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -839,6 +1046,20 @@ __global__ void __launch_bounds__(512, 1)
 }  // namespace nsnkv
 
 using namespace nsnkv;
+
+#ifdef NSNKV_TRACE
+// copy the per-warp timelines (16 x 4096 records) to the host and clear them
+extern "C" int nsnkv_debug_trace(unsigned long long *host, int max_records, int reset) {
+  cudaDeviceSynchronize();
+  const int n = 16 * 4096 < max_records ? 16 * 4096 : max_records;
+  if (host && n) cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n);
+  if (reset) {
+    static unsigned long long zero[16 * 4096];
+    cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
+  }
+  return n;
+}
+#endif
 
 template <int G, bool FOLD, int PREC>
 int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, float *lse,

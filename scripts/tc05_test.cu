@@ -12,7 +12,9 @@
 using namespace nsnkv;
 constexpr int M = 128, N = 16, K = 128;
 
-__global__ void k(const __half *A, const __half *B, float *out1, float *out2) {
+__device__ long long g_cyc[4];
+template <bool MN>
+__global__ void k(const __half *A, const __half *B, float *out1, float *out2, uint32_t p_sb) {
   __shared__ __align__(1024) uint8_t bsm[K * N * 2];
   __shared__ uint32_t tbase;
   __shared__ __align__(8) uint64_t bar;
@@ -22,7 +24,10 @@ __global__ void k(const __half *A, const __half *B, float *out1, float *out2) {
   for (int i = tid; i < K * N; i += blockDim.x) {
     const int kk = i / N, n = i % N;
     const int kt = kk / 16, kh = (kk % 16) / 8, k0 = kk % 8;
-    *reinterpret_cast<__half *>(bsm + kt * 512 + (n / 8) * 256 + kh * 128 + (n % 8) * 16 + k0 * 2) = B[i];
+    if (MN)  // MN-major: element (k, n) at (k/8)*256 + (n/8)*128 + (k%8)*16 + (n%8)*2
+      *reinterpret_cast<__half *>(bsm + (kk / 8) * 256 + (n / 8) * 128 + k0 * 16 + (n % 8) * 2) = B[i];
+    else
+      *reinterpret_cast<__half *>(bsm + kt * 512 + (n / 8) * 256 + kh * 128 + (n % 8) * 16 + k0 * 2) = B[i];
   }
   if (warp == 0) {
     tc05::alloc((uint32_t)__cvta_generic_to_shared(&tbase), 128);
@@ -55,9 +60,49 @@ __global__ void k(const __half *A, const __half *B, float *out1, float *out2) {
   tc05::fence_after();
   if (tid == 0) {
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bsm);
+    // issue cost of 16 back-to-back MMAs (accumulating into column 64.. so
+    // the checked result below is unaffected), then time to completion
+    {
+      const long long c0 = clock64();
+      for (int kt = 0; kt < 16; ++kt)
+        tc05::mma_f16_ts(tb + 96, tb + 16 + 8 * (kt & 7),
+                         MN ? tc05::smem_desc(sb + 512 * (kt & 7), 256, 128) : tc05::smem_desc(sb + 512 * (kt & 7), 128, 256),
+                         tc05::idesc_f16(M, N) | (MN ? (1u << 16) : 0u), kt > 0);
+      const long long c1 = clock64();
+      tc05::commit((uint32_t)__cvta_generic_to_shared(&bar));
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tW0:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, 1000000;\n\t"
+          "@!p bra W0;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(&bar))
+          : "memory");
+      const long long c2 = clock64();
+      g_cyc[0] = c1 - c0;
+      g_cyc[1] = c2 - c0;
+    }
+    if (sb == p_sb && tb == 0) {  // operands provably uniform: kernel parameter + constants
+      const long long c0 = clock64();
+#pragma unroll
+      for (int kt = 0; kt < 16; ++kt)
+        tc05::mma_f16_ts(96, 16 + 8 * (kt & 7),
+                         MN ? tc05::smem_desc(p_sb + 512 * (kt & 7), 256, 128) : tc05::smem_desc(p_sb + 512 * (kt & 7), 128, 256),
+                         tc05::idesc_f16(M, N) | (MN ? (1u << 16) : 0u), kt > 0);
+      const long long c1 = clock64();
+      tc05::commit((uint32_t)__cvta_generic_to_shared(&bar));
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tW1:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 1, 1000000;\n\t"
+          "@!p bra W1;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(&bar))
+          : "memory");
+      const long long c2 = clock64();
+      g_cyc[2] = c1 - c0;
+      g_cyc[3] = c2 - c0;
+    } else {
+      g_cyc[2] = -1; g_cyc[3] = (long long)sb * 1000000 + tb;
+    }
     for (int kt = 0; kt < 8; ++kt)
-      tc05::mma_f16_ts(tb + 0, tb + 16 + 8 * kt, tc05::smem_desc(sb + 512 * kt, 128, 256),
-                       tc05::idesc_f16(M, N), kt > 0);
+      tc05::mma_f16_ts(tb + 0, tb + 16 + 8 * kt,
+                       MN ? tc05::smem_desc(sb + 512 * kt, 256, 128) : tc05::smem_desc(sb + 512 * kt, 128, 256),
+                       tc05::idesc_f16(M, N) | (MN ? (1u << 16) : 0u), kt > 0);
     tc05::commit((uint32_t)__cvta_generic_to_shared(&bar));
   }
   asm volatile(
@@ -104,8 +149,10 @@ int main() {
   cudaMalloc(&d2, M * N * 4);
   cudaMemcpy(dA, hA, M * K * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, hB, K * N * 2, cudaMemcpyHostToDevice);
+  for (int mn = 0; mn < 2; ++mn) {
   cudaMemset(d2, 0xff, M * N * 4);
-  k<<<1, 128>>>(dA, dB, d1, d2);
+  unsigned sbh = (unsigned)atoi(getenv("SB") ? getenv("SB") : "1024");
+  if (mn) k<true><<<1, 128>>>(dA, dB, d1, d2, sbh); else k<false><<<1, 128>>>(dA, dB, d1, d2, sbh);
   cudaError_t e = cudaDeviceSynchronize();
   printf("kernel: %s\n", cudaGetErrorString(e));
   float o1[M * N], o2[M * N];
@@ -120,7 +167,11 @@ int main() {
       e2 = fmax(e2, fabs(ref - o2[m * N + n]));
       mx = fmax(mx, fabs(ref));
     }
-  printf("max|ref| %.3f  err(32x32b) %.3e  err(16x256b) %.3e  %s\n", mx, e1, e2,
+  long long cyc[4];
+  cudaMemcpyFromSymbol(cyc, g_cyc, sizeof(cyc));
+  printf("16 MMA (M128 N16 K16, A tmem): issue %lld cycles, issue+complete %lld cycles; uniform operands: issue %lld, +complete %lld\n", cyc[0], cyc[1], cyc[2], cyc[3]);
+  printf("%s max|ref| %.3f  err(32x32b) %.3e  err(16x256b) %.3e  %s\n", mn ? "MN-major" : "K-major", mx, e1, e2,
          (e1 < 1e-3 && e2 < 1e-3) ? "PASS" : "FAIL");
+  }
   return 0;
 }
