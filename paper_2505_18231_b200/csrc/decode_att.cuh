@@ -195,6 +195,44 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
     int c1 = (int)(x1 * grid / total_chunks);
     while (c1 + 1 < grid && range_lo(total_chunks, c1 + 1, grid) <= x1) ++c1;
     while (c1 > 0 && range_lo(total_chunks, c1, grid) > x1) --c1;
+    if (ALLREC) {
+      // every (CTA, group) slot of the unit holds a record (m = -inf when
+      // empty): load them in batches of 8 with independent loads, then merge
+      const int nrec = (c1 - c0 + 1) * NGRP;
+      for (int r0 = 0; r0 < nrec; r0 += 8) {
+        float rm8 = -INFINITY, rl8 = 0.f;
+        if (lane < 8 && r0 + lane < nrec) {
+          const int r = r0 + lane, c = c0 + r / NGRP, gq = r % NGRP;
+          const float *rec = record_ptr<G>(const_cast<float *>(recs), (u + c) * NGRP + gq) + h * (4 + D);
+          rm8 = rec[0];
+          rl8 = rec[1];
+        }
+        float4 r4[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          r4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (r0 + i < nrec) {
+            const int r = r0 + i, c = c0 + r / NGRP, gq = r % NGRP;
+            const float *rec = record_ptr<G>(const_cast<float *>(recs), (u + c) * NGRP + gq) + h * (4 + D);
+            r4[i] = *reinterpret_cast<const float4 *>(rec + 4 + 4 * lane);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float rm = __shfl_sync(0xffffffffu, rm8, i);
+          const float rl = __shfl_sync(0xffffffffu, rl8, i);
+          if (!(rm > -INFINITY)) continue;  // the group saw no chunk of this unit
+          const float mn = fmaxf(m, rm);
+          const float sa = exp2f(m - mn), sb = exp2f(rm - mn);
+          a.x = a.x * sa + r4[i].x * sb;
+          a.y = a.y * sa + r4[i].y * sb;
+          a.z = a.z * sa + r4[i].z * sb;
+          a.w = a.w * sa + r4[i].w * sb;
+          l = l * sa + rl * sb;
+          m = mn;
+        }
+      }
+    } else
     for (int c = c0; c <= c1; ++c) {
       // local chunk indices of unit u inside CTA c; group gq owns k % NGRP == gq
       const int64_t clo = range_lo(total_chunks, c, grid);

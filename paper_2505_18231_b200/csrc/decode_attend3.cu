@@ -34,6 +34,10 @@
 #include "decode_att.cuh"
 #include "tc05.cuh"
 
+#ifndef NSNKV_SINGLE_STREAM
+#define NSNKV_SINGLE_STREAM 1
+#endif
+
 namespace nsnkv {
 
 #ifdef NSNKV_TRACE
@@ -334,6 +338,60 @@ __global__ void __launch_bounds__(512, 1)
 
     constexpr int NSLOT = C::NSLOT, NZB = C::NZB;
     if (warp == 12) {
+#if NSNKV_SINGLE_STREAM
+      // ---------------- warp 12: page streaming (single in-order stream) --------
+      // payload (idx [+ signs]) of every item into the main ring with 16-byte
+      // cp.async from all 32 lanes (a few outstanding 1-D bulk copies per SM
+      // cannot keep HBM busy); every lane's completion arrives on the stage's
+      // full barrier (cp.async.mbarrier.arrive.noinc, 32 arrivals).  Page ids
+      // come from 32-entry windows of the page table loaded by all lanes at once.
+      {
+        constexpr uint32_t MB = (uint32_t)C::MAIN;
+        constexpr int V16 = C::MAIN / 16 / 32;  // 16-byte vectors per lane per page
+        int wu = -1, wc0 = 0;
+        int32_t wv = 0;
+        Item3 tit = start;
+        for (int k = 0; tit.x < hi; ++k) {
+          const int gk = k % NGRP, nk = k / NGRP;
+          const int s2 = gk * C::NS + nk % C::NS;
+          const int cnt2 = item3_count<CP>(tit);
+          int64_t pg[CP];
+#pragma unroll
+          for (int q = 0; q < CP; ++q) {
+            const int c = tit.c + (q < cnt2 ? q : 0);
+            if (tit.u != wu || c < wc0 || c >= wc0 + 32) {
+              wu = tit.u;
+              wc0 = c;
+              const int cc = c + lane;
+              wv = cc < tit.end ? cv.page_table[(int64_t)tit.u * cv.page_table_stride + cc] : 0;
+            }
+            pg[q] = (int64_t)__shfl_sync(0xffffffffu, wv, c - wc0);
+          }
+          if (nk >= C::NS) mbar_wait_sleep(&BR.empty[s2], (uint32_t)((nk / C::NS) - 1) & 1u);
+          const uint32_t st2 = smem_u32(ring + s2 * C::STAGE);
+#pragma unroll
+          for (int q = 0; q < CP; ++q) {
+            if (q < cnt2) {
+              const uint8_t *ks = cv.k_pool + pg[q] * PB, *vs = cv.v_pool + pg[q] * PB;
+#pragma unroll
+              for (int v = 0; v < V16; ++v) {
+                const uint32_t o = (uint32_t)(16 * (lane + 32 * v));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + o),
+                             "l"(ks + o)
+                             : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + MB + o),
+                             "l"(vs + o)
+                             : "memory");
+              }
+            }
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&BR.full[s2]))
+                       : "memory");
+          A3_TRACE(12, 0, k);
+          item3_next<CP>(tit, hi, cv.n_chunks, n_units);
+        }
+      }
+#else
       // ---------------- warp 12: page streaming --------------------------------
       // payload (idx [+ signs]) of every item into its group's ring (NS stages
       // per group: no head-of-line blocking between groups) with 16-byte
@@ -408,6 +466,7 @@ __global__ void __launch_bounds__(512, 1)
           if (!progress) __nanosleep(256);
         }
       }
+#endif
     } else {
       // ---------------- item producer of group gp ------------------------------
       const int gp = warp - 13;
