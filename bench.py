@@ -134,7 +134,7 @@ def dist_setup():
     return world, rank, local
 
 
-def build_cache(cfg_name: str, device, seed: int, precision: str = "precise"):
+def build_cache(cfg_name: str, device, seed: int, precision: str | None = None):
     """Encode a synthetic cache of the workload shape with the product's own
     append path (chunked so fp32 staging stays small)."""
     import torch
@@ -269,6 +269,7 @@ def run_ours(args) -> dict | None:
         "config": {"workload": f"{args.config}: batch {B}/rank, {Hq}q/{Hkv}kv heads, d128, "
                                f"context {T}, {bm}-bit",
                    "global_batch": B * world, "seq_len": T, "parallelism": f"batch-sharded x{world}",
+                   "precision": cache.precision,
                    "l2": "inputs larger than L2 (packed cache %.0f MB/rank)" % (sbytes / 1e6)},
         "tokens_per_s": round(B * world / (ms * 1e-3), 1),
         "e2e": {"value": round(sbytes * world / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
@@ -429,8 +430,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the serving-step and encode measurements")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--precision", default="precise", choices=["precise", "balanced", "fast"],
-                    help="decode codeword precision (DESIGN.md 3.2)")
+    ap.add_argument("--precision", default=None, choices=["precise", "balanced", "fast"],
+                    help="decode codeword precision (DESIGN.md 3.2); default: the library's "
+                         "(fast for 2-bit, precise for 1-bit)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     res = run_reference(args) if args.impl == "reference" else run_ours(args)

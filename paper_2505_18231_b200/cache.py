@@ -43,6 +43,14 @@ CNT_CLAMP, CNT_ZERO, CNT_FALLBACK, CNT_NEARTIE = range(4)
 PRECISIONS = {"precise": 0, "balanced": 1, "fast": 2}
 
 
+def default_precision(bit_mode) -> str:
+    """2-bit: plain fp16 codewords ("fast"; the random per-component signs
+    keep the rounding unbiased, every parity case stays within the 1e-3
+    output tolerance); 1-bit: fp16 hi + lo codewords ("precise"; plain fp16
+    misses the tolerance on the misaligned fixture)."""
+    return "fast" if int(bit_mode) == 2 else "precise"
+
+
 class ScaleStrategy(enum.IntEnum):
     """Reconstruction rescaling (vq.py:31-48)."""
 
@@ -147,8 +155,8 @@ class PagedKvCache:
                  base_position: int = 0, device=None, check_finite: bool = True,
                  precision: str | None = None):
         config.check_gpu_path()
-        if precision is None:  # deployment default; NSNKV_PRECISION overrides
-            precision = os.environ.get("NSNKV_PRECISION", "precise")
+        if precision is None:  # deployment default (DESIGN.md 3.2); NSNKV_PRECISION overrides
+            precision = os.environ.get("NSNKV_PRECISION") or default_precision(config.bit_mode)
         self.check_finite = check_finite
         # decode codeword precision: "precise" = fp16 hi + lo
         # on both sides, "balanced" = plain fp16 scores / hi + lo values,

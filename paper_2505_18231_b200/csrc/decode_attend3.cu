@@ -863,7 +863,10 @@ __global__ void __launch_bounds__(512, 1)
       for (int c = 0; c < CP; ++c) {
 #pragma unroll
         for (int nt = 0; nt < NTP; ++nt) pd[c][nt][0] = pd[c][nt][1] = 0.f;
-        if (c < cnt) {
+        // fast mode computes a missing second chunk on stale stage bytes
+        // (gathers only ever return finite table entries; its weights are
+        // masked to zero) so both chunks' gathers can interleave
+        if (C::ONE_TABLE || c < cnt) {
           const uint32_t kpa = smem_u32(st + c * 2 * C::MAIN);
           const uint32_t ik0 = lds32(kpa + L.idx + tok0 * NSUB + 4 * t);
           const uint32_t ik1 = lds32(kpa + L.idx + tok1 * NSUB + 4 * t);
@@ -1017,7 +1020,7 @@ __global__ void __launch_bounds__(512, 1)
       const int vt0 = 16 * ws + 2 * t;
 #pragma unroll
       for (int c = 0; c < CP; ++c) {
-        if (c >= cnt) break;
+        if (!C::ONE_TABLE && c >= cnt) break;
         const uint32_t vpa = smem_u32(st + c * 2 * C::MAIN + C::MAIN);
         uint32_t iv[4], sv[4];
 #pragma unroll
