@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libnsnkv_b200.so"
 
-SOURCES = ["capi.cu", "level1.cu", "encode.cu", "decode_ref.cu", "decode_attend.cu", "decode_attend2.cu", "decode_attend3.cu", "decode_ws.cu"]
+SOURCES = ["capi.cu", "level1.cu", "encode.cu", "decode_ref.cu", "decode_attend.cu", "decode_attend3.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1,5 +1,5 @@
 // decode_att.cuh -- PTX helpers, chunk cursor, stream-K records and the
-// combine kernel shared by the decode kernels (decode_attend.cu, decode_ws.cu).
+// combine kernel shared by the decode kernels (decode_attend.cu, decode_attend3.cu).
 #pragma once
 #include "common.cuh"
 #include "decode_common.cuh"
@@ -318,15 +318,7 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
 
 }  // namespace nsnkv
 
-// warp-specialized decode launcher (decode_ws.cu), instantiated for G = 1, 2, 4
-template <int G, bool FOLD, int PREC>
-int nsnkv_launch_attend_ws(const nsnkv::CacheViewDev &cv, const float *q, float *out, float *lse,
-                           float *recs, int64_t total, int grid, cudaStream_t st);
 
-// second-generation decode launcher (decode_attend2.cu), G = 1, 2, 4, 8
-template <int G, bool FOLD, int PREC>
-int nsnkv_launch_attend2(const nsnkv::CacheViewDev &cv, const float *q, float *out, float *lse,
-                         float *recs, int64_t total, int grid, cudaStream_t st);
 
 // warp-specialized decode launcher (decode_attend3.cu), G = 1, 2, 4, 8
 template <int G, bool FOLD, int PREC>

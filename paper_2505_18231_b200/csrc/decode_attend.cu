@@ -628,15 +628,13 @@ extern "C" size_t nsnkv_decode_workspace_bytes(const nsnkv_cache_view *cv_in) {
 }
 
 // Kernel selection (NSNKV_DECODE_KERNEL): "v3" (default) the warp-specialized
-// kernel with the shift term on tcgen05 (decode_attend3.cu); "v2" the paired
-// grouped kernel (decode_attend2.cu); "v1" the first-generation grouped
-// kernel below; "ws" the first-generation warp-specialized variant.
+// kernel with the shift term on tcgen05 (decode_attend3.cu); "v1" the
+// first-generation grouped kernel below (kept for A/B measurements).
 static int decode_kernel_choice() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("NSNKV_DECODE_KERNEL");
-    v = (e && strcmp(e, "ws") == 0) ? 0 : (e && strcmp(e, "v1") == 0) ? 1
-      : (e && strcmp(e, "v2") == 0) ? 2 : 3;
+    v = (e && strcmp(e, "v1") == 0) ? 1 : 3;
   }
   return v;
 }
@@ -648,17 +646,6 @@ static int launch_attend(const CacheViewDev &cv, const float *q, float *out, flo
     int grid = attend_grid();
     if (total < grid) grid = (int)(total > 0 ? total : 1);
     return nsnkv_launch_attend3<G, FOLD, PREC>(cv, q, out, lse, recs, total, grid, st);
-  }
-  if (decode_kernel_choice() == 2) {
-    int grid = attend_grid();
-    if (total < grid) grid = (int)(total > 0 ? total : 1);
-    return nsnkv_launch_attend2<G, FOLD, PREC>(cv, q, out, lse, recs, total, grid, st);
-  }
-  if (G <= 4 && decode_kernel_choice() == 0) {  // warp-specialized kernel (decode_ws.cu)
-    int grid = attend_grid();
-    if (total < grid) grid = (int)(total > 0 ? total : 1);
-    return nsnkv_launch_attend_ws<(G <= 4 ? G : 4), FOLD, PREC>(cv, q, out, lse, recs, total,
-                                                                 grid, st);
   }
   static bool attr = false;
   if (!attr) {

@@ -34,9 +34,6 @@
 #include "decode_att.cuh"
 #include "tc05.cuh"
 
-#ifndef NSNKV_SINGLE_STREAM
-#define NSNKV_SINGLE_STREAM 1
-#endif
 
 namespace nsnkv {
 
@@ -272,13 +269,13 @@ __global__ void __launch_bounds__(512, 1)
     tc05::relinquish();
     if (lane == 0) {
       for (int s = 0; s < NSTAGE; ++s) {
-        mbar_init(&BR.full[s], 32);  // the streaming warp's lanes (cp.async arrivals)
-        mbar_init(&BR.empty[s], 4);  // the group's 4 consumer warps
+        mbar_init(&BR.full[s], 1);  // the streaming thread's expect_tx arrive
+        mbar_init(&BR.empty[s], 128);  // every thread of the group's 4 consumer warps
       }
       for (int q = 0; q < NGRP; ++q)
         for (int s = 0; s < C::NSLOT; ++s) {
-          mbar_init(&BR.ready[q][s], 2);  // the group's producer + the MMA commit
-          mbar_init(&BR.free_[q][s], 4);
+          mbar_init(&BR.ready[q][s], 33);  // the producer warp's lanes + the MMA commit
+          mbar_init(&BR.free_[q][s], 128);  // every consumer thread of the group
         }
       mbar_init(&BR.tabs, C::ONE_TABLE ? 128 : 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -338,16 +335,13 @@ __global__ void __launch_bounds__(512, 1)
 
     constexpr int NSLOT = C::NSLOT, NZB = C::NZB;
     if (warp == 12) {
-#if NSNKV_SINGLE_STREAM
-      // ---------------- warp 12: page streaming (single in-order stream) --------
-      // payload (idx [+ signs]) of every item into the main ring with 16-byte
-      // cp.async from all 32 lanes (a few outstanding 1-D bulk copies per SM
-      // cannot keep HBM busy); every lane's completion arrives on the stage's
-      // full barrier (cp.async.mbarrier.arrive.noinc, 32 arrivals).  Page ids
-      // come from 32-entry windows of the page table loaded by all lanes at once.
+      // ---------------- warp 12: page streaming ---------------------------------
+      // payload (idx [+ signs]) of every item, in item order, into its group's
+      // ring (NS stages per group) with 1-D bulk copies (TMA engine).  Page ids
+      // come from 32-entry windows of the page table loaded by all lanes at
+      // once (one load latency per 32 chunks).
       {
         constexpr uint32_t MB = (uint32_t)C::MAIN;
-        constexpr int V16 = C::MAIN / 16 / 32;  // 16-byte vectors per lane per page
         int wu = -1, wc0 = 0;
         int32_t wv = 0;
         Item3 tit = start;
@@ -368,105 +362,19 @@ __global__ void __launch_bounds__(512, 1)
             pg[q] = (int64_t)__shfl_sync(0xffffffffu, wv, c - wc0);
           }
           if (nk >= C::NS) mbar_wait_sleep(&BR.empty[s2], (uint32_t)((nk / C::NS) - 1) & 1u);
-          const uint32_t st2 = smem_u32(ring + s2 * C::STAGE);
-#pragma unroll
-          for (int q = 0; q < CP; ++q) {
-            if (q < cnt2) {
-              const uint8_t *ks = cv.k_pool + pg[q] * PB, *vs = cv.v_pool + pg[q] * PB;
-#pragma unroll
-              for (int v = 0; v < V16; ++v) {
-                const uint32_t o = (uint32_t)(16 * (lane + 32 * v));
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + o),
-                             "l"(ks + o)
-                             : "memory");
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + MB + o),
-                             "l"(vs + o)
-                             : "memory");
-              }
+          if (lane == 0) {
+            uint8_t *st2 = ring + s2 * C::STAGE;
+            mbar_expect_tx(&BR.full[s2], (uint32_t)cnt2 * 2u * MB);
+            for (int q = 0; q < cnt2; ++q) {
+              tma_load_1d(st2 + q * 2 * MB, cv.k_pool + pg[q] * PB, MB, &BR.full[s2]);
+              tma_load_1d(st2 + q * 2 * MB + MB, cv.v_pool + pg[q] * PB, MB, &BR.full[s2]);
             }
           }
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&BR.full[s2]))
-                       : "memory");
+          __syncwarp();
           A3_TRACE(12, 0, k);
           item3_next<CP>(tit, hi, cv.n_chunks, n_units);
         }
       }
-#else
-      // ---------------- warp 12: page streaming --------------------------------
-      // payload (idx [+ signs]) of every item into its group's ring (NS stages
-      // per group: no head-of-line blocking between groups) with 16-byte
-      // cp.async from all 32 lanes; every lane's completion arrives on the
-      // stage's full barrier (cp.async.mbarrier.arrive.noinc, 32 arrivals).
-      // Page ids come from 32-entry windows of the page table (per group).
-      {
-        constexpr uint32_t MB = (uint32_t)C::MAIN;
-        constexpr int V16 = C::MAIN / 16 / 32;  // 16-byte vectors per lane per page
-        constexpr int NS = C::NS;
-        int wu[NGRP], wc0[NGRP], nis[NGRP];
-        int32_t wv[NGRP];
-        Item3 tc[NGRP];
-        {
-          Item3 x = start;
-#pragma unroll
-          for (int g = 0; g < NGRP; ++g) {
-            tc[g] = x;
-            item3_next<CP>(x, hi, cv.n_chunks, n_units);
-            wu[g] = -1, wc0[g] = 0, wv[g] = 0, nis[g] = 0;
-          }
-        }
-        for (;;) {
-          bool any = false, progress = false;
-#pragma unroll
-          for (int g = 0; g < NGRP; ++g) {
-            if (tc[g].x >= hi) continue;
-            any = true;
-            const int n = nis[g], s2 = g * NS + n % NS;
-            bool ok = n < NS;
-            if (!ok) ok = __shfl_sync(0xffffffffu, lane == 0 ? (int)mbar_test(&BR.empty[s2], (uint32_t)((n / NS) - 1) & 1u) : 0, 0);
-            if (!ok) continue;
-            const Item3 &it2 = tc[g];
-            const int cnt2 = item3_count<CP>(it2);
-            int64_t pg[CP];
-#pragma unroll
-            for (int q = 0; q < CP; ++q) {
-              const int c = it2.c + (q < cnt2 ? q : 0);
-              if (it2.u != wu[g] || c < wc0[g] || c >= wc0[g] + 32) {
-                wu[g] = it2.u;
-                wc0[g] = c;
-                const int cc = c + lane;
-                wv[g] = cc < it2.end ? cv.page_table[(int64_t)it2.u * cv.page_table_stride + cc] : 0;
-              }
-              pg[q] = (int64_t)__shfl_sync(0xffffffffu, wv[g], c - wc0[g]);
-            }
-            const uint32_t st2 = smem_u32(ring + s2 * C::STAGE);
-#pragma unroll
-            for (int q = 0; q < CP; ++q) {
-              if (q < cnt2) {
-                const uint8_t *ks = cv.k_pool + pg[q] * PB, *vs = cv.v_pool + pg[q] * PB;
-#pragma unroll
-                for (int v = 0; v < V16; ++v) {
-                  const uint32_t o = (uint32_t)(16 * (lane + 32 * v));
-                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + o),
-                               "l"(ks + o)
-                               : "memory");
-                  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(st2 + q * 2 * MB + MB + o),
-                               "l"(vs + o)
-                               : "memory");
-                }
-              }
-            }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&BR.full[s2]))
-                         : "memory");
-            A3_TRACE(12, 0, 3 * n + g);
-            for (int a = 0; a < NGRP; ++a) item3_next<CP>(tc[g], hi, cv.n_chunks, n_units);
-            ++nis[g];
-            progress = true;
-          }
-          if (!any) break;
-          if (!progress) __nanosleep(256);
-        }
-      }
-#endif
     } else {
       // ---------------- item producer of group gp ------------------------------
       const int gp = warp - 13;
@@ -646,8 +554,8 @@ __global__ void __launch_bounds__(512, 1)
         tc05::fence_proxy_async();
         __syncwarp();
         A3_TRACE(warp, 5, n);
+        mbar_arrive(&BR.ready[gp][slot]);  // every lane: its scales and value shift vectors
         if (lane == 0) {
-          mbar_arrive(&BR.ready[gp][slot]);  // scales and value shift vectors
           if (e == BATCH - 1 || nx.x >= hi) {  // issue the batch's shift-term MMA chain
             tc05::fence_after();
             const int nf = m * BATCH;          // first item of the batch
@@ -1083,11 +991,8 @@ __global__ void __launch_bounds__(512, 1)
       // release the stage and the producer slot (scales, value shifts, TMEM D)
       A3_TRACE(warp, 4, n);
       tc05::fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&BR.empty[s]);
-        mbar_arrive(&BR.free_[grp][slot]);
-      }
+      mbar_arrive(&BR.empty[s]);
+      mbar_arrive(&BR.free_[grp][slot]);
       for (int a = 0; a < NGRP; ++a) item3_next<CP>(cur, hi, cv.n_chunks, n_units);
     }
     if (cur_unit >= 0) {

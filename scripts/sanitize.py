@@ -10,11 +10,11 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2505_18231_b200 as P  # noqa: E402
 from paper_2505_18231_b200 import kernels  # noqa: E402
 
-for mode, G in (("2b", 4), ("1b", 1), ("2b", 8)):
+for mode, G, prec in (("2b", 4, "fast"), ("2b", 4, "precise"), ("1b", 1, None), ("2b", 8, None)):
     cb = P.default_codebook(mode)
     cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
     B, H, T = 2, 2, 64 * 5 + 9
-    c = P.PagedKvCache(cfg, B, H, cb_k=cb, cb_v=cb)
+    c = P.PagedKvCache(cfg, B, H, cb_k=cb, cb_v=cb, precision=prec)
     x = torch.randn(B, H, T, 128, device="cuda")
     c.append(x, x)
     q = torch.randn(B, H * G, 128, device="cuda")
@@ -23,7 +23,7 @@ for mode, G in (("2b", 4), ("1b", 1), ("2b", 8)):
     w = torch.softmax(s.double() / 128 ** 0.5, -1).float()
     out2 = c.output(w)
     torch.cuda.synchronize()
-    print(mode, G, float((out - out2).abs().max()))
+    print(mode, G, c.precision, float((out - out2).abs().max()))
 v = np.random.default_rng(0).standard_normal((3000, 8)).astype(np.float32)
 e = np.abs(np.random.default_rng(1).standard_normal((256, 8)).astype(np.float32)) + np.float32(0.01)
 kernels.match_block(v, e, kernels.entry_inv_norms(e), True)
