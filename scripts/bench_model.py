@@ -185,7 +185,7 @@ def main():
         "batch": args.batch, "context": args.context, "layers": args.layers,
         "ms_per_step": round(ms, 3), "tokens_per_s": round(args.batch / (ms * 1e-3), 1),
         "kv_cache_GB": round(kv_bytes / 1e9, 2), "max_mem_GB": round(torch.cuda.max_memory_allocated() / 1e9, 1),
-        "build_s": round(build_s, 1), "precision": args.precision if args.kv != "bf16" else "bf16",
+        "build_s": round(build_s, 1), "precision": (caches[0].precision if caches else "bf16"),
     }), flush=True)
 
 
