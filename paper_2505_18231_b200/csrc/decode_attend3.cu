@@ -760,7 +760,14 @@ __global__ void __launch_bounds__(512, 1)
       const int cnt = item3_count<CP>(cur);
       const int s = grp * C::NS + n % C::NS, slot = n % C::NSLOT;
       A3_TRACE(warp, 0, n);
-      mbar_wait(&BR.full[s], (uint32_t)(n / C::NS) & 1u);
+      // page data: back off with nanosleep instead of spinning (a spinning
+      // waiter wakes on every barrier event of the CTA and takes issue slots
+      // from the consumer warps that have data)
+      if (!mbar_test(&BR.full[s], (uint32_t)(n / C::NS) & 1u)) {
+        do {
+          __nanosleep(128);
+        } while (!mbar_test(&BR.full[s], (uint32_t)(n / C::NS) & 1u));
+      }
       A3_TRACE(warp, 1, n);
       const uint8_t *st = ring + s * C::STAGE;
 
