@@ -46,12 +46,13 @@ def needs_rebuild() -> bool:
 
 def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
     """trace=True builds libnsnkv_b200_trace.so with -DNSNKV_TRACE (a debug
-    timeline of CTA 0 in the decode kernel, scripts/trace_decode.py)."""
-    lib = LIB.with_name("libnsnkv_b200_trace.so") if trace else LIB
+    timeline of CTA 0 in the decode kernel, scripts/trace_decode.py).
+    NSNKV_EXTRA_FLAGS / NSNKV_LIB_NAME build experiment variants next to it."""
     extra = os.environ.get("NSNKV_EXTRA_FLAGS", "").split()
+    lib = LIB.with_name("libnsnkv_b200_trace.so") if trace else LIB
     if extra:
         lib = lib.with_name(os.environ.get("NSNKV_LIB_NAME", lib.name))
-    if not force and not trace and not needs_rebuild():
+    if not force and not trace and not extra and not needs_rebuild():
         return LIB
     cmd = [nvcc(), *NVCC_FLAGS, *(["-DNSNKV_TRACE"] if trace else []), *extra, "-I", str(ROOT / "include"),
            *[str(CSRC / s) for s in SOURCES], "-o", str(lib) + ".tmp", "-lcudart"]

@@ -71,10 +71,14 @@ struct A3 {
   static constexpr int TAILS = CP * 2 * META;  // producer's staged page tails per item
   static constexpr bool ONE_TABLE = PREC == 2;     // K hi | V hi interleaved per entry
   static constexpr int TBL = ONE_TABLE ? 65536 : 131072;
-  static constexpr int ZB = 4096 * (ONE_TABLE ? 2 : 1);  // B operand: K 128 x N fp16
-  static constexpr int NSLOT = ONE_TABLE ? 4 : 2;  // producer -> consumer item slots
+#ifndef NSNKV_FAST_BATCH
+#define NSNKV_FAST_BATCH 2
+#endif
+  static constexpr int FB = ONE_TABLE ? NSNKV_FAST_BATCH : 1;
+  static constexpr int ZB = 4096 * FB;             // B operand: K 128 x N fp16
+  static constexpr int NSLOT = ONE_TABLE ? (FB == 2 ? 4 : 3) : 2;  // producer -> consumer item slots
   static constexpr int NZB = 1;                    // shift-term B operand buffers per group
-  static constexpr int BATCH = ONE_TABLE ? 2 : 1;  // items per shift-term MMA chain
+  static constexpr int BATCH = FB;                 // items per shift-term MMA chain
   static constexpr int NB = 16 * BATCH;            // MMA N: (item, chunk, head, Z hi/lo)
 
   struct Slot {
@@ -771,6 +775,13 @@ __global__ void __launch_bounds__(512, 1)
       A3_TRACE(warp, 1, n);
       const uint8_t *st = ring + s * C::STAGE;
 
+#ifdef NSNKV_DEBUG_SKIP_CONSUME
+      // pipeline-ceiling experiment: wait for the producer slot, skip all math
+#ifndef NSNKV_DEBUG_SKIP_READY
+      mbar_wait(&BR.ready[grp][slot], (uint32_t)(n / C::NSLOT) & 1u);
+#endif
+      if (false) {
+#endif
       // ---- K side: payload dot products on tensor cores ----------------------
       const int tok0 = 16 * ws + g, tok1 = tok0 + 8;
       float pd[CP][NTP][2];
@@ -995,6 +1006,9 @@ __global__ void __launch_bounds__(512, 1)
           }
         }
       }
+#ifdef NSNKV_DEBUG_SKIP_CONSUME
+      }
+#endif
       // release the stage and the producer slot (scales, value shifts, TMEM D)
       A3_TRACE(warp, 4, n);
       tc05::fence_before();

@@ -18,6 +18,12 @@
 namespace nsnkv {
 
 constexpr int ENC_THREADS = 256;
+// resident CTAs per SM the register budget is sized for: the phases of a
+// chunk are separated by block barriers, so a third CTA keeps the SM busy
+// while the other two wait (80 registers, a few bytes of spill)
+#ifndef ENC_MIN_BLOCKS
+#define ENC_MIN_BLOCKS 3
+#endif
 constexpr int XS = D + 4;  // padded smem row stride (floats)
 
 struct EncodeSmem {
@@ -128,7 +134,7 @@ __device__ __forceinline__ uint32_t rtn4_level(float v, float zero32f, float sca
 }
 
 template <bool FOLD>
-__global__ void __launch_bounds__(ENC_THREADS, 2) encode_chunks_kernel(
+__global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_kernel(
     const float *__restrict__ residual, int n_resid, const void *__restrict__ fresh, int fresh_bf16,
     int64_t n_fresh, int n_flush, int is_key, const int64_t *__restrict__ start_pos,
     const float2 *__restrict__ rope_cs, int64_t rope_pos0, int64_t rope_n, CodebookDev cb,
