@@ -272,31 +272,30 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
       A[m][2] = pack_h2(l0, l1);  // row g,   K cols 2t+8..2t+9: u_lo
       A[m][3] = pack_h2(l2, l3);  // row g+8
     }
+    // top-2 of packed keys: the score's fp32 bits with the low 8 mantissa bits
+    // replaced by the entry index (a perturbation below 2^-15 |score|, added
+    // to the near-tie bound), so max / min carry the index along
     float best[4][2], sec[4][2];
-    int bi[4][2];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        best[m][r] = sec[m][r] = -3.0e38f;
-        bi[m][r] = 0;
-      }
+      for (int r = 0; r < 2; ++r) best[m][r] = sec[m][r] = -3.0e38f;
 #pragma unroll 2
     for (int nt = 0; nt < 32; ++nt) {
       const uint2 bb = s.mb[nt][lane];
-      const int c0 = 8 * nt + 2 * lt;
+      const uint32_t c0 = (uint32_t)(8 * nt + 2 * lt);
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         float d[4] = {0.f, 0.f, 0.f, 0.f};
         mma16816(d, A[m][0], A[m][1], A[m][2], A[m][3], bb.x, bb.x);
         mma16816(d, A[m][0], A[m][1], A[m][2], A[m][3], bb.y, 0u);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = q >> 1;
-          const float v = d[q];
-          sec[m][r] = fmaxf(sec[m][r], fminf(best[m][r], v));
-          if (v > best[m][r]) bi[m][r] = c0 + (q & 1);
-          best[m][r] = fmaxf(best[m][r], v);
+        for (int r = 0; r < 2; ++r) {
+          const float a = __uint_as_float((__float_as_uint(d[2 * r]) & 0xffffff00u) | c0);
+          const float b = __uint_as_float((__float_as_uint(d[2 * r + 1]) & 0xffffff00u) | (c0 + 1));
+          const float mx = fmaxf(a, b), mn = fminf(a, b);
+          sec[m][r] = fmaxf(sec[m][r], fmaxf(fminf(best[m][r], mx), mn));
+          best[m][r] = fmaxf(best[m][r], mx);
         }
       }
     }
@@ -309,13 +308,12 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
         for (int off = 1; off <= 2; off <<= 1) {
           const float ob = __shfl_xor_sync(0xffffffffu, best[m][r], off);
           const float os = __shfl_xor_sync(0xffffffffu, sec[m][r], off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi[m][r], off);
           sec[m][r] = fmaxf(fminf(best[m][r], ob), fmaxf(sec[m][r], os));
-          if (ob > best[m][r] || (ob == best[m][r] && oi < bi[m][r])) bi[m][r] = oi;
           best[m][r] = fmaxf(best[m][r], ob);
         }
       }
     // decide: lane lt owns token m = lt of this pass (rows g and g + 8)
+    uint32_t need = 0;  // bit r: row r of this lane's token needs the exact pass
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       if (m != lt) continue;
@@ -327,26 +325,74 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
         uint8_t res = 0;
         if (!((zm >> sub) & 1u)) {
           const float sb = best[m][r], ss = sec[m][r];
-          float u[8];
           float n2 = 0.f;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const float v = s.x[tau][8 * sub + k];
-            u[k] = (FOLD && v < 0.f) ? -v : v;
-            n2 = fmaf(u[k], u[k], n2);
+            n2 = fmaf(v, v, n2);
           }
           // fp16 hi + lo operands (2^-22 each) with fp32 tensor-core
-          // accumulation: |score error| < 2^-19 * ||u||; 4x margin
-          const float bound = 2.0f * 7.6293945e-06f * sqrtf(n2);  // 2 * 2^-17 * ||u||
-          const bool ok = n2 > 1e-24f && n2 < 1e30f && ss < sb - bound;
-          if (ok) {
-            res = (uint8_t)bi[m][r];
-          } else {
-            res = (uint8_t)match_exact_fp64(u, s.ent, s.inv);
-            ++slow;
-          }
+          // accumulation: |score error| < 2^-19 * ||u|| (4x margin: 2^-17),
+          // plus the index bits of both keys (< 2^-15 * ||u|| each)
+          const float bound = (2.0f * 7.6293945e-06f + 2.0f * 3.0517578e-05f) * sqrtf(n2);
+          if (n2 > 1e-24f && n2 < 1e30f && ss < sb - bound && fabsf(sb) > 1e-30f)
+            res = (uint8_t)(__float_as_uint(sb) & 0xffu);
+          else
+            need |= 1u << r;
         }
         s.idx[tau][sub] = res;
+      }
+    }
+    // near ties: the whole warp re-scores one sub-vector at a time exactly in
+    // fp64 (the reference loop: component-order sum, times inv[c], strict '>'
+    // from -1e300 so the lowest index wins ties); lane l scores entries
+    // l, l + 32, ..., then an argmax butterfly with the lower index on ties
+    for (uint32_t pend = __ballot_sync(0xffffffffu, need != 0); pend;
+         pend = __ballot_sync(0xffffffffu, need != 0)) {
+      const int src = __ffs(pend) - 1;
+      const uint32_t nb = __shfl_sync(0xffffffffu, need, src);
+      const int r = __ffs(nb) - 1;
+      const int tau = 8 * warp + 4 * hf + (src & 3), sub = (src >> 2) + 8 * r;
+      double ud[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float v = s.x[tau][8 * sub + k];
+        ud[k] = (double)((FOLD && v < 0.f) ? -v : v);
+      }
+      double bs = -1e300;
+      int bc = 0;
+#pragma unroll 2
+      for (int i = 0; i < NENT / 32; ++i) {
+        const int c = 32 * i + lane;
+        const float4 e0 = *reinterpret_cast<const float4 *>(&s.ent[8 * c]);
+        const float4 e1 = *reinterpret_cast<const float4 *>(&s.ent[8 * c + 4]);
+        double sc = __dmul_rn(ud[0], (double)e0.x);
+        sc = __dadd_rn(sc, __dmul_rn(ud[1], (double)e0.y));
+        sc = __dadd_rn(sc, __dmul_rn(ud[2], (double)e0.z));
+        sc = __dadd_rn(sc, __dmul_rn(ud[3], (double)e0.w));
+        sc = __dadd_rn(sc, __dmul_rn(ud[4], (double)e1.x));
+        sc = __dadd_rn(sc, __dmul_rn(ud[5], (double)e1.y));
+        sc = __dadd_rn(sc, __dmul_rn(ud[6], (double)e1.z));
+        sc = __dadd_rn(sc, __dmul_rn(ud[7], (double)e1.w));
+        sc = __dmul_rn(sc, s.inv[c]);
+        if (sc > bs) {
+          bs = sc;
+          bc = c;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, bs, off);
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
+        if (os > bs || (os == bs && oc < bc)) {
+          bs = os;
+          bc = oc;
+        }
+      }
+      if (lane == src) {
+        s.idx[tau][sub] = (uint8_t)bc;
+        need &= ~(1u << r);
+        ++slow;
       }
     }
   }
