@@ -146,3 +146,31 @@ def test_rope_table_matches_numpy():
     ref = orc.rope_table(n)
     mism = int((got != ref).sum())
     assert mism <= 2, f"{mism} float32 cos/sin values differ from numpy"
+
+
+@pytest.mark.parametrize("case", list(pipeline_inputs()), ids=[c[0] for c in PIPELINE_CASES])
+def test_fused_precision_modes_vs_reference(case):
+    """Every decode precision mode usable for the case's bit mode (DESIGN.md
+    §3.2) stays within the north-star output tolerance of the reference on
+    every golden case, including the misaligned fixtures."""
+    import torch
+
+    import paper_2505_18231_b200 as P
+
+    g = load_golden(f"pipeline_{case['name']}.npz")
+    cb = codebook_for(case["bit_mode"])
+    # 1-bit: plain fp16 scores miss the tolerance on the misaligned fixture
+    # (1.25e-3), so only "precise" is offered as a 1-bit default
+    modes = ("precise",) + (("balanced", "fast") if cb.bit_mode == 2 else ())
+    for prec in modes:
+        cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode, strategy=P.ScaleStrategy(case["strategy"]))
+        c = P.PagedKvCache(cfg, 1, 1, cb_k=cb, cb_v=cb, base_position=case["base_position"],
+                           precision=prec)
+        for a, b in case["batches"]:
+            c.append(torch.from_numpy(case["keys"][a:b][None, None]).cuda(),
+                     torch.from_numpy(case["values_ht"][a:b][None, None]).cuda())
+        out = c.attend(torch.from_numpy(case["q"][None]).cuda()).cpu().numpy()[0]
+        for i in range(len(case["q"])):
+            ref_o = g["out"][i]
+            err = np.max(np.abs(out[i] - ref_o))
+            assert err <= OUT_TOL * np.max(np.abs(ref_o)), (prec, i, err)
