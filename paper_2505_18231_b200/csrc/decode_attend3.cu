@@ -535,14 +535,14 @@ __global__ void __launch_bounds__(512, 1)
                   al = qv.x * he + qv.y * ho;
                   be = qv.y * he - qv.x * ho;
                 }
-                // hi = fp16 (al, be), lo = fp16 of the remainders
-                const __half2 hh2 = __floats2half2_rn(al, be);
-                const float2 hf = __half22float2(hh2);
-                const __half2 lh2 = __floats2half2_rn(al - hf.x, be - hf.y);
-                const uint32_t hw = *reinterpret_cast<const uint32_t *>(&hh2);
-                const uint32_t lw = *reinterpret_cast<const uint32_t *>(&lh2);
-                ra[hh] = prmt(hw, lw, 0x5410u);  // (a hi, a lo)
-                rb[hh] = prmt(hw, lw, 0x7632u);  // (b hi, b lo)
+                // hi = the top 11 significant bits (exact in fp16), lo = the
+                // exact fp32 remainder rounded to fp16: |error| < 2^-21 |x|
+                const float ah = __uint_as_float(__float_as_uint(al) & 0xffffe000u);
+                const float bh = __uint_as_float(__float_as_uint(be) & 0xffffe000u);
+                const __half2 pa = __floats2half2_rn(ah, al - ah);
+                const __half2 pb = __floats2half2_rn(bh, be - bh);
+                ra[hh] = *reinterpret_cast<const uint32_t *>(&pa);  // (a hi, a lo)
+                rb[hh] = *reinterpret_cast<const uint32_t *>(&pb);  // (b hi, b lo)
               }
               const int n1 = (CP == 2 ? c : hg) + 2 * e;
               const uint32_t row = zb_s + (uint32_t)((j >> 2) * (NB * 16) + n1 * 128 + (j & 3) * 32);
@@ -555,12 +555,15 @@ __global__ void __launch_bounds__(512, 1)
             }
           }
         }
-        tc05::fence_proxy_async();
+        // Z stores become visible to the tensor core (async proxy) before the
+        // batch's MMA chain; one fence per batch covers both items' stores
+        const bool issue = e == BATCH - 1 || nx.x >= hi;
+        if (issue) tc05::fence_proxy_async();
         __syncwarp();
         A3_TRACE(warp, 5, n);
         mbar_arrive(&BR.ready[gp][slot]);  // every lane: its scales and value shift vectors
         if (lane == 0) {
-          if (e == BATCH - 1 || nx.x >= hi) {  // issue the batch's shift-term MMA chain
+          if (issue) {  // issue the batch's shift-term MMA chain
             tc05::fence_after();
             const int nf = m * BATCH;          // first item of the batch
             const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (NSLOT * gp + nf % NSLOT));
