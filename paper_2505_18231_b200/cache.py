@@ -219,6 +219,16 @@ class PagedKvCache:
                            + torch.arange(new, device=dev, dtype=torch.int32)[None, :]).contiguous()
         self.max_chunks = new
 
+    def reserve(self, max_tokens: int) -> "PagedKvCache":
+        """Pre-size the page pools and the RoPE table for contexts up to
+        max_tokens per unit, so later appends never grow them (a growth
+        reallocates and copies the pools: a server reserves up front)."""
+        n = (int(max_tokens) + R - 1) // R
+        if n > self.max_chunks:
+            self._reserve_chunks(n)
+        self.rope.ensure(self.base_position + n * R)
+        return self
+
     @property
     def n_quantized(self) -> int:
         return self.n_chunks * R

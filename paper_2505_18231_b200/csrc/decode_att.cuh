@@ -261,17 +261,31 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
   const int nres = cv.n_res[u];
   if (nres > 0) {
     const int64_t pbase = cv.base_pos[u] + (int64_t)nch * R;
-    for (int tt = lane; tt < nres; tt += 32) {
-      const float *kr = cv.k_res + ((int64_t)u * R + tt) * D;
-      const float2 *cs = cv.rope_cs + (pbase + tt - cv.rope_pos0) * NPAIR;
-      float acc = 0.f;
-      for (int j = 0; j < NPAIR; ++j) {
-        const float2 e = cs[j];
-        const float ke = kr[2 * j], ko = kr[2 * j + 1];
-        acc = fmaf(ke * e.x - ko * e.y, s_q[wr][2 * j], acc);
-        acc = fmaf(ke * e.y + ko * e.x, s_q[wr][2 * j + 1], acc);
+    // warp-cooperative: lane l rotates and multiplies channels 4l .. 4l+3
+    // (pairs 2l, 2l+1) of 8 rows at a time (coalesced row loads), then one
+    // butterfly per row
+    for (int t0 = 0; t0 < nres; t0 += 8) {
+      float part[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        part[i] = 0.f;
+        const int tt = t0 + i;
+        if (tt < nres) {
+          const float4 k4 = *reinterpret_cast<const float4 *>(cv.k_res + ((int64_t)u * R + tt) * D + 4 * lane);
+          const float4 c4 = *reinterpret_cast<const float4 *>(
+              cv.rope_cs + (pbase + tt - cv.rope_pos0) * NPAIR + 2 * lane);
+          const float re0 = k4.x * c4.x - k4.y * c4.y, ro0 = k4.x * c4.y + k4.y * c4.x;
+          const float re1 = k4.z * c4.z - k4.w * c4.w, ro1 = k4.z * c4.w + k4.w * c4.z;
+          part[i] = fmaf(ro1, q4.w, fmaf(re1, q4.z, fmaf(ro0, q4.y, re0 * q4.x)));
+        }
       }
-      s_w[wr][tt] = acc * LOG2E_OVER_SQRTD;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) part[i] += __shfl_xor_sync(0xffffffffu, part[i], o);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (lane == i && t0 + i < nres) s_w[wr][t0 + i] = part[i] * LOG2E_OVER_SQRTD;
     }
     __syncwarp();
     float rm = -INFINITY;
@@ -280,6 +294,7 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
     const float sa = (m > -INFINITY) ? exp2f(m - mn) : 0.f;
     a.x *= sa; a.y *= sa; a.z *= sa; a.w *= sa;
     l *= sa;
+#pragma unroll 8
     for (int tt = 0; tt < nres; ++tt) {
       const float p = exp2f(s_w[wr][tt] - mn);
       const float4 v4 = *reinterpret_cast<const float4 *>(cv.v_res + ((int64_t)u * R + tt) * D + 4 * lane);
