@@ -46,6 +46,27 @@ def test_decode_fill_equals_prefill(mode):
     assert torch.equal(pre.attend(q), dec.attend(q))
 
 
+def test_reserve_presizes_and_keeps_results():
+    """reserve() sizes the pools once; appends up to the reserved length never
+    reallocate, and the cache contents equal an unreserved cache's."""
+    B, H, T = 2, 2, 64 * 5 + 3
+    g = torch.Generator(device="cuda")
+    g.manual_seed(4)
+    k = torch.randn(B, H, T, 128, device="cuda", generator=g)
+    v = torch.randn(B, H, T, 128, device="cuda", generator=g)
+    a = _cache("2b", B, H).reserve(T)
+    pools = (a.k_pool.data_ptr(), a.v_pool.data_ptr(), a.max_chunks)
+    b = _cache("2b", B, H)
+    for i in range(0, T, 7):
+        a.append(k[:, :, i:i + 7], v[:, :, i:i + 7])
+        b.append(k[:, :, i:i + 7], v[:, :, i:i + 7])
+    assert (a.k_pool.data_ptr(), a.v_pool.data_ptr(), a.max_chunks) == pools
+    for u in range(B * H):
+        assert a.snapshot(u) == b.snapshot(u)
+    q = torch.randn(B, 4 * H, 128, device="cuda", generator=g)
+    assert torch.equal(a.attend(q), b.attend(q))
+
+
 def test_chunk_counting_and_residual():
     # reference test_kvcache.py:35-50: 130 tokens -> 2 chunks + 2 residual rows
     c = _cache("2b", 1, 1)
