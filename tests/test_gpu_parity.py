@@ -174,3 +174,36 @@ def test_fused_precision_modes_vs_reference(case):
             ref_o = g["out"][i]
             err = np.max(np.abs(out[i] - ref_o))
             assert err <= OUT_TOL * np.max(np.abs(ref_o)), (prec, i, err)
+
+
+@pytest.mark.parametrize("mode", ["1b", "2b"])
+def test_encode_exact_ties_vs_oracle(mode):
+    """Codebooks with duplicated and rescaled entries make exact and
+    last-bit cosine ties everywhere (reference tie rule: the lowest index
+    wins, test_kernels_parity.py:41-54).  Every such sub-vector goes through
+    the encode kernel's warp-cooperative fp64 pass; the pages must still be
+    bit-identical to the oracle's chunks."""
+    import torch
+
+    import paper_2505_18231_b200 as P
+    from oracle import oracle as orc
+
+    base = codebook_for(int(mode[0]))
+    e = base.entries.copy()
+    e[1::2] = e[0::2]                                   # exact duplicates: 128 tie pairs
+    e[2:64:4] = e[0:62:4] * np.float32(1.0000001)       # same direction, other norm
+    cb = P.Codebook(entries=e, bit_mode=base.bit_mode)
+    cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
+    B, H, T = 1, 2, 64 * 3
+    rng = np.random.default_rng(3)
+    k = rng.standard_normal((B, H, T, 128)).astype(np.float32)
+    v = rng.standard_normal((B, H, T, 128)).astype(np.float32)
+    cache = P.PagedKvCache(cfg, B, H, cb_k=cb, cb_v=cb)
+    cache.append(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda())
+    near_ties = int(cache.counters()[:, 3].sum())
+    assert near_ties > 0
+    for u in range(B * H):
+        oc = orc.OracleCache(cb.entries, cb.entries, int(cb.bit_mode))
+        oc.append(k[0, u], v[0, u])
+        assert cache.chunk_wire(u, "k") == oc.k_chunks
+        assert cache.chunk_wire(u, "v") == oc.v_chunks
