@@ -133,6 +133,15 @@ __device__ __forceinline__ uint32_t rtn4_level(float v, float zero32f, float sca
   return (uint32_t)lv;
 }
 
+// D += A (16 x 8, fp16, row) . B (8 x 8, fp16, col), fp32 accumulate
+__device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+
 template <bool FOLD>
 __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_kernel(
     const float *__restrict__ residual, int n_resid, const void *__restrict__ fresh, int fresh_bf16,
@@ -245,11 +254,10 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
     __syncwarp();
   }
   // (b) tensor-core pre-pass: scores[sub][c] = u . e_c / ||e_c|| with u and
-  // the normalized entries split into fp16 hi + lo (mma.sync m16n8k16: K =
-  // [u_hi | u_lo] against [e_hi ; e_hi], then [u_hi | u_lo] against
-  // [e_lo ; 0]).  One m-tile = the 16 sub-vectors of one token; warp w takes
-  // tokens 8w .. 8w+7.  Scores are tracked as packed (score | 255 - c) keys
-  // with top-2 per sub-vector; a sub-vector whose runner-up is within the
+  // the normalized entries split into fp16 hi + lo (three mma.sync m16n8k8:
+  // u_hi.e_hi + u_lo.e_hi + u_hi.e_lo).  One m-tile = the 16 sub-vectors of
+  // one token; warp w takes tokens 8w .. 8w+7.  Scores are tracked as packed
+  // (score bits | index c) keys with top-2 per sub-vector; a sub-vector whose runner-up is within the
   // error bound is re-scored exactly in fp64 (the reference loop).
   int slow = 0;
 #pragma unroll 1
@@ -282,21 +290,32 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
       for (int r = 0; r < 2; ++r) best[m][r] = sec[m][r] = -3.0e38f;
 #pragma unroll 2
     for (int nt = 0; nt < 32; ++nt) {
+      // three m16n8k8 products u_hi.e_hi + u_lo.e_hi + u_hi.e_lo: each B
+      // operand is one register as loaded (no pair copies)
       const uint2 bb = s.mb[nt][lane];
-      const uint32_t c0 = (uint32_t)(8 * nt + 2 * lt);
+      const uint32_t c0 = (uint32_t)(8 * nt + 2 * lt), c1 = c0 | 1u;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        mma16816(d, A[m][0], A[m][1], A[m][2], A[m][3], bb.x, bb.x);
-        mma16816(d, A[m][0], A[m][1], A[m][2], A[m][3], bb.y, 0u);
+      for (int mp = 0; mp < 4; mp += 2) {  // two m-tiles interleaved: no back-to-back dependent MMAs
+      float dd[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int i = 0; i < 2; ++i) mma1688(dd[i], A[mp + i][0], A[mp + i][1], bb.x);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) mma1688(dd[i], A[mp + i][2], A[mp + i][3], bb.x);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) mma1688(dd[i], A[mp + i][0], A[mp + i][1], bb.y);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int m = mp + i;
+        const float(&d)[4] = dd[i];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const float a = __uint_as_float((__float_as_uint(d[2 * r]) & 0xffffff00u) | c0);
-          const float b = __uint_as_float((__float_as_uint(d[2 * r + 1]) & 0xffffff00u) | (c0 + 1));
+          const float b = __uint_as_float((__float_as_uint(d[2 * r + 1]) & 0xffffff00u) | c1);
           const float mx = fmaxf(a, b), mn = fminf(a, b);
           sec[m][r] = fmaxf(sec[m][r], fmaxf(fminf(best[m][r], mx), mn));
           best[m][r] = fmaxf(best[m][r], mx);
         }
+      }
       }
     }
     // merge the top-2 lists of the four lanes sharing a sub-vector (same g)
