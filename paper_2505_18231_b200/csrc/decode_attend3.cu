@@ -500,6 +500,9 @@ __global__ void __launch_bounds__(512, 1)
         // coefficient b_j) and n = 8 (chunk | head group) + 2 head + (hi | lo):
         // each (j, chunk) writes two 16-byte rows (a_j and b_j for 4 heads x hi/lo);
         // lanes 4..7 of every 8 store the b row first (conflict-free phases)
+#ifdef NSNKV_DEBUG_SKIP_Z  // pipeline-ceiling experiment: no Z work (wrong results)
+        if (false)
+#endif
 #pragma unroll
         for (int c = 0; c < CP; ++c) {
           float osc = 0.f, oz = 0.f, osc2 = 0.f, oz2 = 0.f;
