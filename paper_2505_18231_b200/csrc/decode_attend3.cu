@@ -419,6 +419,38 @@ __global__ void __launch_bounds__(512, 1)
       uint4 tl0[2], tl1[2];  // tails of items n and n + 1
       tail_load(it, tl0);
       tail_load(it1, tl1);
+      // the address operands of those prefetches (page id of this lane's tail,
+      // the unit's base position) are loaded one item earlier still, so no
+      // prefetch waits on a dependent load inside the loop
+      auto pid_load = [&](const Item3 &x) -> int32_t {
+        const int c = lane >> 4;
+        if (x.x >= hi || c >= item3_count<CP>(x)) return 0;
+        return cv.page_table[(int64_t)x.u * cv.page_table_stride + x.c + c];
+      };
+      auto tail_load_p = [&](const Item3 &x, int32_t page, uint4 (&r)[2]) {
+        r[0] = r[1] = make_uint4(0, 0, 0, 0);
+        if (x.x >= hi) return;
+        const int t = lane >> 3, c = t >> 1;
+        if (c >= item3_count<CP>(x)) return;
+        const uint8_t *src = ((t & 1) ? cv.v_pool : cv.k_pool) + (int64_t)page * PB + C::MAIN + 32 * (lane & 7);
+        r[0] = __ldg(reinterpret_cast<const uint4 *>(src));
+        r[1] = __ldg(reinterpret_cast<const uint4 *>(src + 16));
+      };
+      auto rope_rows_p = [&](const Item3 &x, int64_t bp, float2 (&r)[CP][2]) {
+        if (x.x >= hi) return;
+        const int cnt = item3_count<CP>(x);
+        const int64_t pb = bp - cv.rope_pos0;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+          const int64_t p0 = pb + (int64_t)(x.c + (c < cnt ? c : 0)) * R;
+          r[c][0] = __ldg(cv.rope_cs + p0 * NPAIR + lane);
+          r[c][1] = __ldg(cv.rope_cs + p0 * NPAIR + lane + 32);
+        }
+      };
+      Item3 it2 = it1;
+      for (int a = 0; a < NGRP; ++a) item3_next<CP>(it2, hi, cv.n_chunks, n_units);
+      int32_t pid2 = pid_load(it2);
+      int64_t bp1 = it1.x < hi ? cv.base_pos[it1.u] : 0;
       int n = 0;
       for (int k = gp; it.x < hi; k += NGRP, ++n) {
         const int cnt = item3_count<CP>(it);
@@ -435,12 +467,14 @@ __global__ void __launch_bounds__(512, 1)
                                 : make_float2(0.f, 0.f);
         }
         Item3 nx = it1;  // next item of this producer: prefetch its RoPE rows
+        Item3 it3 = it2;  // three items ahead: its tail's page id
+        for (int a = 0; a < NGRP; ++a) item3_next<CP>(it3, hi, cv.n_chunks, n_units);
+        const int32_t pid3 = pid_load(it3);
+        const int64_t bp2 = it2.x < hi ? cv.base_pos[it2.u] : 0;
         float2 rcs_next[CP][2];
-        rope_rows(nx, rcs_next);
-        Item3 it2 = it1;  // two items ahead: prefetch its page tails
-        for (int a = 0; a < NGRP; ++a) item3_next<CP>(it2, hi, cv.n_chunks, n_units);
-        uint4 tl2[2];
-        tail_load(it2, tl2);
+        rope_rows_p(nx, bp1, rcs_next);
+        uint4 tl2[2];  // two items ahead: its page tails
+        tail_load_p(it2, pid2, tl2);
         A3_TRACE(warp, 0, n);
         if (n >= NSLOT) mbar_wait_sleep(&BR.free_[gp][slot], (uint32_t)((n / NSLOT) - 1) & 1u);
         A3_TRACE(warp, 1, n);
@@ -583,6 +617,9 @@ __global__ void __launch_bounds__(512, 1)
         A3_TRACE(warp, 6, n);
         it = nx;
         it1 = it2;
+        it2 = it3;
+        pid2 = pid3;
+        bp1 = bp2;
         tl0[0] = tl1[0], tl0[1] = tl1[1];
         tl1[0] = tl2[0], tl1[1] = tl2[1];
 #pragma unroll
