@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(512, 1)
       int n = 0;
       for (int k = gp; it.x < hi; k += NGRP, ++n) {
         const int cnt = item3_count<CP>(it);
-        const int s = k % NSTAGE, slot = n % NSLOT;
+        const int slot = n % NSLOT;
         if (it.u != cur_unit) {
           cur_unit = it.u;
           const int qb = it.u / cv.n_kv_heads, qhk = it.u - qb * cv.n_kv_heads;
@@ -484,7 +484,10 @@ __global__ void __launch_bounds__(512, 1)
         *reinterpret_cast<uint4 *>(P.tails + 32 * lane + 16) = tl0[1];
         __syncwarp();
         A3_TRACE(warp, 2, n);
-        const uint8_t *st = P.tails - C::MAIN;
+        const uint8_t *st = P.tails;
+        // tail field offsets (the page layout's minus the payload size)
+        constexpr PageLayout LT{L.idx, L.sgn, L.s2 - C::MAIN, L.s1n - C::MAIN, L.on - C::MAIN,
+                                L.par - C::MAIN, L.ledger - C::MAIN, L.bytes - C::MAIN};
         constexpr uint32_t TP = 2u * C::META;  // chunk stride in the staged tails
         typename C::Slot &SL = P.slot[slot];
         // token scales (rtn4 s1, f16 s2) of tokens 2 lane, 2 lane + 1, keys and values
@@ -494,11 +497,11 @@ __global__ void __launch_bounds__(512, 1)
           float4 o4 = v0;
           if (c < cnt) {
             const uint8_t *kp = st + c * TP, *vp = kp + C::META;
-            const uint32_t pk01 = *reinterpret_cast<const uint32_t *>(kp + L.par);  // s1 scale, zero
-            const uint32_t pv01 = *reinterpret_cast<const uint32_t *>(vp + L.par);
-            const uint32_t nk = kp[L.s1n + lane], nv = vp[L.s1n + lane];
-            const uint32_t s2k = *reinterpret_cast<const uint32_t *>(kp + L.s2 + 4 * lane);
-            const uint32_t s2v = *reinterpret_cast<const uint32_t *>(vp + L.s2 + 4 * lane);
+            const uint32_t pk01 = *reinterpret_cast<const uint32_t *>(kp + LT.par);  // s1 scale, zero
+            const uint32_t pv01 = *reinterpret_cast<const uint32_t *>(vp + LT.par);
+            const uint32_t nk = kp[LT.s1n + lane], nv = vp[LT.s1n + lane];
+            const uint32_t s2k = *reinterpret_cast<const uint32_t *>(kp + LT.s2 + 4 * lane);
+            const uint32_t s2v = *reinterpret_cast<const uint32_t *>(vp + LT.s2 + 4 * lane);
             const float ksc = f16_bits_to_f32(pk01 & 0xffffu), kz = f16_bits_to_f32(pk01 >> 16);
             const float vsc = f16_bits_to_f32(pv01 & 0xffffu), vz = f16_bits_to_f32(pv01 >> 16);
             const float s1k0 = rtn4(nk & 15u, kz, ksc), s1k1 = rtn4(nk >> 4, kz, ksc);
@@ -509,9 +512,9 @@ __global__ void __launch_bounds__(512, 1)
             v1 = make_float4(s1k1 * k21, s1k1, s1v1 * v21, s1v1);
             // value shift vector: channels 4 lane .. 4 lane + 3 (group lane / 8)
             const int gr = lane >> 3;
-            const float zs = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + L.par)[6 + gr]);
-            const float ss = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + L.par)[2 + gr]);
-            const uint32_t b2 = *reinterpret_cast<const uint16_t *>(vp + L.on + 2 * lane);
+            const float zs = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + LT.par)[6 + gr]);
+            const float ss = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(vp + LT.par)[2 + gr]);
+            const uint32_t b2 = *reinterpret_cast<const uint16_t *>(vp + LT.on + 2 * lane);
             o4 = make_float4(rtn4(b2 & 15u, zs, ss), rtn4((b2 >> 4) & 15u, zs, ss),
                              rtn4((b2 >> 8) & 15u, zs, ss), rtn4((b2 >> 12) & 15u, zs, ss));
           }
@@ -543,13 +546,13 @@ __global__ void __launch_bounds__(512, 1)
           uint32_t ob0 = 0, ob1 = 0;
           if (c < cnt) {
             const uint8_t *kp = st + c * TP;
-            const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + L.par);
+            const uint16_t *pk = reinterpret_cast<const uint16_t *>(kp + LT.par);
             osc = f16_bits_to_f32(pk[2 + (lane >> 4)]);      // group of channels 2 lane
             oz = f16_bits_to_f32(pk[6 + (lane >> 4)]);
             osc2 = f16_bits_to_f32(pk[2 + 2 + (lane >> 4)]); // channels 2 (lane + 32)
             oz2 = f16_bits_to_f32(pk[6 + 2 + (lane >> 4)]);
-            ob0 = kp[L.on + lane];
-            ob1 = kp[L.on + lane + 32];
+            ob0 = kp[LT.on + lane];
+            ob1 = kp[LT.on + lane + 32];
           }
 #pragma unroll
           for (int jj = 0; jj < 2; ++jj) {
