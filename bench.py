@@ -47,6 +47,8 @@ CONFIGS = {
     "c2_1b": (16, 32, 8, 32768, 1),
     "c1": (1, 8, 8, 4096, 1),
     "c4": (128, 32, 8, 131072, 2),
+    # not a BASELINE config: GQA group 8 (LLaMA-3-70B head shape), for coverage
+    "c2_g8": (16, 64, 8, 32768, 2),
 }
 
 
