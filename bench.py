@@ -72,7 +72,8 @@ def measured_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region (NVML
+    every millisecond; nvidia-smi every 100 ms when NVML is unavailable)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -81,10 +82,47 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.source = None
+        self._nvml = self._nvml_open()
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_open(self):
+        """NVML handle opened before the timed region (init takes tens of ms)."""
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+            return pynvml, h, mx, bits
+        except Exception:
+            return None
+
+    def _run_nvml(self) -> bool:
+        """Fast path: NVML polled every millisecond, so a timed region of a
+        few milliseconds still gets several samples (at least one)."""
+        if self._nvml is None:
+            return False
+        pynvml, h, mx, bits = self._nvml
+        self.source = "nvml"
+        while True:
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+            except Exception:
+                pass
+            if self._stop.wait(0.001):
+                break
+        return True
+
     def _run(self):
+        if self._run_nvml():
+            return
+        self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -117,7 +155,7 @@ class ClockSampler:
                           if s[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": self.source}
 
 
 def dist_setup():
@@ -446,7 +484,10 @@ def run_reference(args) -> dict | None:
         return None
     B, Hq, Hkv, T, bm = CONFIGS[args.config]
     vals = []
-    step_budget = float(os.environ.get("NSNKV_REF_STEP_S", "3"))  # seconds of CPU work per step
+    # seconds of CPU work per step: 3 s, less when many steps are asked for so
+    # the whole run stays within ~2.5 minutes
+    step_budget = float(os.environ.get("NSNKV_REF_STEP_S", "3"))
+    step_budget = max(0.2, min(step_budget, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         cpu_baseline(args.config, budget_s=step_budget)
     for _ in range(args.steps):
@@ -468,7 +509,7 @@ def run_reference(args) -> dict | None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
