@@ -172,6 +172,11 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
     int64_t total_chunks, int grid, float *__restrict__ out, float *__restrict__ lse) {
   __shared__ __align__(16) float s_q[COMBINE_ROWS][D];
   __shared__ float s_w[COMBINE_ROWS][R];
+  // G >= COMBINE_ROWS: the CTA's rows are q-heads of one unit, so the rotated
+  // residual keys are staged once per CTA (row stride D + 1: conflict-free
+  // when lane t reads row t)
+  constexpr bool SHARED_RES = G >= COMBINE_ROWS;
+  __shared__ float s_kr[SHARED_RES ? R : 1][D + 1];
   const int wr = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * COMBINE_ROWS + wr;
   if (row >= cv.batch * cv.n_q_heads) return;
@@ -261,6 +266,30 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
   const int nres = cv.n_res[u];
   if (nres > 0) {
     const int64_t pbase = cv.base_pos[u] + (int64_t)nch * R;
+    if constexpr (SHARED_RES) {
+      // every thread of the CTA rotates a share of the rows (coalesced loads,
+      // all in flight together), then lane t scores row t against its q-head
+      for (int idx = threadIdx.x; idx < nres * (D / 4); idx += 32 * COMBINE_ROWS) {
+        const int tt = idx / (D / 4), l4 = idx - tt * (D / 4);
+        const float4 k4 = *reinterpret_cast<const float4 *>(cv.k_res + ((int64_t)u * R + tt) * D + 4 * l4);
+        const float4 c4 = *reinterpret_cast<const float4 *>(
+            cv.rope_cs + (pbase + tt - cv.rope_pos0) * NPAIR + 2 * l4);
+        float *kr = &s_kr[tt][4 * l4];
+        kr[0] = k4.x * c4.x - k4.y * c4.y;
+        kr[1] = k4.x * c4.y + k4.y * c4.x;
+        kr[2] = k4.z * c4.z - k4.w * c4.w;
+        kr[3] = k4.z * c4.w + k4.w * c4.z;
+      }
+      __syncthreads();
+      for (int tt = lane; tt < nres; tt += 32) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};  // four independent chains
+#pragma unroll 8
+        for (int d = 0; d < D; d += 4)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] = fmaf(s_kr[tt][d + e], s_q[wr][d + e], acc[e]);
+        s_w[wr][tt] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * LOG2E_OVER_SQRTD;
+      }
+    } else {
     // warp-cooperative: lane l rotates and multiplies channels 4l .. 4l+3
     // (pairs 2l, 2l+1) of 8 rows at a time (coalesced row loads), then one
     // butterfly per row
@@ -286,6 +315,7 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (lane == i && t0 + i < nres) s_w[wr][t0 + i] = part[i] * LOG2E_OVER_SQRTD;
+    }
     }
     __syncwarp();
     float rm = -INFINITY;
