@@ -9,8 +9,9 @@
 //
 // Roles (512 threads, one CTA per SM, stream-K split of the chunk list into
 // work items of CP consecutive chunks of one unit):
-//  * warp 12 (TMA): streams each item's K and V pages into a shared-memory
-//    ring with 1-D bulk copies (cp.async.bulk + mbarrier complete_tx);
+//  * warp 12 (TMA): streams each item's K and V page payloads, in item order,
+//    into its group's shared-memory ring with 1-D bulk copies
+//    (cp.async.bulk + mbarrier complete_tx);
 //  * warps 13..15 (item producers, one per consumer group): per item, the
 //    token scales, the value shift vectors and the shift-term B operand
 //    Z[(cos,sin)_j][(chunk, head, hi/lo)] = q . RoPE(o, p0) (split hi + lo
@@ -18,7 +19,8 @@
 //    tensor cores:  D[tau][n] = Tab[tau][(cos,sin)_j] . Z  with the constant
 //    Tab = (cos, sin)(tau f_j) resident in TMEM as fp16 hi + lo stacked along
 //    M (8 tcgen05.mma, M = 128 = 64 positions x hi/lo, N = 16 = 2 chunks x 4
-//    heads x Z hi/lo, A from TMEM, B from shared memory), accumulator in TMEM;
+//    heads x Z hi/lo, A from TMEM, B from shared memory; `fast` chains two
+//    items, N = 32), accumulator in TMEM;
 //  * warps 0..11 (3 consumer groups of 4 warps; warp ws owns token positions
 //    [16 ws, 16 ws + 16) of every chunk): codeword gathers from 64 KB-aligned
 //    shared-memory tables, sign flips, K-side payload products and V-side
