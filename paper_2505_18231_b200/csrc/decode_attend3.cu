@@ -492,6 +492,10 @@ __global__ void __launch_bounds__(512, 1)
                                 L.par - C::MAIN, L.ledger - C::MAIN, L.bytes - C::MAIN};
         constexpr uint32_t TP = 2u * C::META;  // chunk stride in the staged tails
         typename C::Slot &SL = P.slot[slot];
+#ifdef NSNKV_DEBUG_SKIP_PRODUCE  // consumer-ceiling experiment: no producer work (wrong results)
+        if (false)
+#endif
+        {
         // token scales (rtn4 s1, f16 s2) of tokens 2 lane, 2 lane + 1, keys and values
 #pragma unroll
         for (int c = 0; c < CP; ++c) {
@@ -524,6 +528,7 @@ __global__ void __launch_bounds__(512, 1)
           SL.sc[c][2 * lane + 1] = v1;
           *reinterpret_cast<float4 *>(&SL.ov[c][4 * lane]) = o4;
         }
+        }
         A3_TRACE(warp, 3, n);
         // the MMA chain that last used this Z buffer (batch m - NZB) is done
         constexpr int BATCH = C::BATCH, NB = C::NB;
@@ -539,7 +544,7 @@ __global__ void __launch_bounds__(512, 1)
         // coefficient b_j) and n = 8 (chunk | head group) + 2 head + (hi | lo):
         // each (j, chunk) writes two 16-byte rows (a_j and b_j for 4 heads x hi/lo);
         // lanes 4..7 of every 8 store the b row first (conflict-free phases)
-#ifdef NSNKV_DEBUG_SKIP_Z  // pipeline-ceiling experiment: no Z work (wrong results)
+#if defined(NSNKV_DEBUG_SKIP_Z) || defined(NSNKV_DEBUG_SKIP_PRODUCE)  // ceiling experiments (wrong results)
         if (false)
 #endif
 #pragma unroll
@@ -610,6 +615,9 @@ __global__ void __launch_bounds__(512, 1)
             const int nf = m * BATCH;          // first item of the batch
             const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (NSLOT * gp + nf % NSLOT));
             constexpr uint32_t idesc = tc05::idesc_f16(128, NB) | (1u << 16);  // B MN-major
+#ifdef NSNKV_DEBUG_SKIP_PRODUCE
+            if (false)
+#endif
 #pragma unroll
             for (int kt = 0; kt < 8; ++kt)
               tc05::mma_f16_ts(dcol, tmem + 8 * kt,
