@@ -1000,6 +1000,9 @@ __global__ void __launch_bounds__(512, 1)
 
       // ---- V side: accumulate P' . codewords on tensor cores -----------------
       const int vt0 = 16 * ws + 2 * t;
+#ifdef NSNKV_DEBUG_SKIP_VSIDE  // cost-split experiment: no value side (wrong results)
+      if (false)
+#endif
 #pragma unroll
       for (int c = 0; c < CP; ++c) {
         if (!C::ONE_TABLE && c >= cnt) break;
