@@ -186,3 +186,21 @@ def test_oracle_builds_with_gcc():
 
     lib = orc.build()
     assert Path(lib).exists()
+
+
+def test_bench_step_bytes_and_clock_summary():
+    """bench.py host logic without a GPU: the algorithmic bytes of the C2
+    step (300.9 MB) and the clock-sample summary
+    (median SM clock, throttle reasons that were active in any sample)."""
+    import bench
+
+    B, Hq, Hkv, T, bm = bench.CONFIGS["c2"]
+    assert bench.step_bytes(B, Hq, Hkv, T, bm) == 300_941_312
+    cs = bench.ClockSampler.__new__(bench.ClockSampler)
+    cs.samples = [["1965", "1965", "Not Active", "Not Active", "Not Active", "Not Active"],
+                  ["1950", "1965", "Not Active", "Not Active", "Not Active", "Active"],
+                  ["1965", "1965", "Not Active", "Not Active", "Not Active", "Not Active"]]
+    cs.source = "nvml"
+    s = cs.summary()
+    assert s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["sw_power_cap"] and s["samples"] == 3
