@@ -73,6 +73,9 @@ struct A3 {
   static constexpr int TAILS = CP * 2 * META;  // producer's staged page tails per item
   static constexpr bool ONE_TABLE = PREC == 2;     // K hi | V hi interleaved per entry
   static constexpr int TBL = ONE_TABLE ? 65536 : 131072;
+#ifndef NSNKV_FULL_SLEEP_NS
+#define NSNKV_FULL_SLEEP_NS 128  // consumer poll interval while its page payload is in flight
+#endif
 #ifndef NSNKV_FAST_BATCH
 #define NSNKV_FAST_BATCH 2
 #endif
@@ -820,14 +823,18 @@ __global__ void __launch_bounds__(512, 1)
       const int cnt = item3_count<CP>(cur);
       const int s = grp * C::NS + n % C::NS, slot = n % C::NSLOT;
       A3_TRACE(warp, 0, n);
-      // page data: back off with nanosleep instead of spinning (a spinning
-      // waiter wakes on every barrier event of the CTA and takes issue slots
-      // from the consumer warps that have data)
+      // page data: mbarrier try_wait (the warp is suspended in hardware until
+      // the phase completes or the time hint expires); measured 1-2 % faster
+      // than polling with nanosleep back-off (-DNSNKV_FULL_SLEEP_POLL)
+#ifndef NSNKV_FULL_SLEEP_POLL
+      mbar_wait(&BR.full[s], (uint32_t)(n / C::NS) & 1u);
+#else
       if (!mbar_test(&BR.full[s], (uint32_t)(n / C::NS) & 1u)) {
         do {
-          __nanosleep(128);
+          __nanosleep(NSNKV_FULL_SLEEP_NS);
         } while (!mbar_test(&BR.full[s], (uint32_t)(n / C::NS) & 1u));
       }
+#endif
       A3_TRACE(warp, 1, n);
       const uint8_t *st = ring + s * C::STAGE;
 
