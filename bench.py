@@ -17,10 +17,13 @@ e2e     same metric through the public API (PagedKvCache.attend) with q
 restatement of the reference algorithm, on all host cores) on a bounded
 sample of the same workload.
 
-Multi-GPU: one process per GPU (torchrun); every rank holds its own batch
-of 16 sequences (weak scaling: the (batch, kv-head) units are independent,
-no collective inside attention); outputs are all-gathered over NCCL at the
-end of each step (the serving layout's only exchange).
+Multi-GPU: one process per GPU (torchrun; ``--gpus N`` re-launches itself
+under torch.distributed.run when WORLD_SIZE is unset).  The (batch, kv-head)
+units are independent, so there is no collective inside attention; outputs are
+all-gathered over NCCL at the end of each step (the serving layout's only
+exchange).  c2 runs weak scaling (16 sequences per rank); c4 runs strong
+scaling (BASELINE config 4: a global batch of 128 split by
+sharding.plan_shards, 128/N sequences per rank).
 """
 
 from __future__ import annotations
@@ -42,14 +45,37 @@ sys.path.insert(0, str(ROOT))
 D, R = 128, 64
 LEDGER = {2: 2292, 1: 1268}
 CONFIGS = {
-    # name: (batch per rank, n_q_heads, n_kv_heads, context, bit_mode)
+    # name: (batch per rank (weak) or global batch (strong), n_q_heads,
+    #        n_kv_heads, context, bit_mode)
     "c2": (16, 32, 8, 32768, 2),
     "c2_1b": (16, 32, 8, 32768, 1),
-    "c1": (1, 8, 8, 4096, 1),
+    "c1": (1, 32, 8, 4096, 1),
     "c4": (128, 32, 8, 131072, 2),
     # not a BASELINE config: GQA group 8 (LLaMA-3-70B head shape), for coverage
     "c2_g8": (16, 64, 8, 32768, 2),
 }
+STRONG = {"c4"}  # global batch fixed, split over the ranks
+
+
+def local_batch(cfg_name: str, world: int) -> int:
+    B = CONFIGS[cfg_name][0]
+    if cfg_name not in STRONG:
+        return B
+    if B % world:
+        raise SystemExit(f"{cfg_name}: global batch {B} does not split over {world} ranks")
+    return B // world
+
+
+def config_dict(cfg_name: str, world: int) -> dict:
+    """The workload description -- identical in both arms (same_config)."""
+    B, Hq, Hkv, T, bm = CONFIGS[cfg_name]
+    strong = cfg_name in STRONG
+    gb = B if strong else B * world
+    return {"workload": f"{cfg_name}: global batch {gb}, {Hq}q/{Hkv}kv heads, d128, context {T}, "
+                        f"{bm}-bit packed KV decode attention (one step = every q-head of every "
+                        f"sequence over the whole packed cache)",
+            "global_batch": gb, "seq_len": T, "bit_mode": bm,
+            "parallelism": f"{'strong' if strong else 'weak'} batch-sharded x{world}"}
 
 
 def step_bytes(B, Hq, Hkv, T, bit_mode) -> int:
@@ -174,30 +200,48 @@ def dist_setup():
     return world, rank, local
 
 
-def build_cache(cfg_name: str, device, seed: int, precision: str | None = None):
-    """Encode a synthetic cache of the workload shape with the product's own
-    append path (chunked so fp32 staging stays small)."""
+def build_cache(cfg_name: str, device, seed: int, precision: str | None = None, world: int = 1):
+    """Encode a synthetic cache of the workload shape (this rank's share)
+    with the product's own append path (chunked so staging stays small)."""
     import torch
 
     import paper_2505_18231_b200 as P
 
-    B, Hq, Hkv, T, bm = CONFIGS[cfg_name]
+    _, Hq, Hkv, T, bm = CONFIGS[cfg_name]
+    B = local_batch(cfg_name, world)
     cb = P.default_codebook(f"{bm}b")
     cfg = P.CacheConfig(d=D, bit_mode=cb.bit_mode)
     cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, device=device,
                            check_finite=False, precision=precision)
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
-    block = 4096
+    block = max(R, min(4096, (1 << 26) // (B * Hkv * D) // R * R))
     done = 0
     while done < T:
         n = min(block, T - done)
-        k = torch.randn(B, Hkv, n, D, device=device, generator=gen)
-        v = torch.randn(B, Hkv, n, D, device=device, generator=gen)
+        k = torch.randn(B, Hkv, n, D, device=device, generator=gen, dtype=torch.bfloat16)
+        v = torch.randn(B, Hkv, n, D, device=device, generator=gen, dtype=torch.bfloat16)
         cache.append(k, v)
         done += n
     torch.cuda.synchronize()
     return cache
+
+
+def time_attend(cache, q, out, steps: int) -> float:
+    """ms per nsnkv_decode_attend call (CUDA events on the launching stream,
+    warm-up first)."""
+    import torch
+
+    for _ in range(3):
+        cache.attend(q, out=out)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record()
+    for _ in range(steps):
+        cache.attend(q, out=out)
+    k1.record()
+    torch.cuda.synchronize()
+    return k0.elapsed_time(k1) / steps
 
 
 def run_ours(args) -> dict | None:
@@ -207,22 +251,26 @@ def run_ours(args) -> dict | None:
 
     world, rank, local = dist_setup()
     device = torch.device("cuda", local)
-    B, Hq, Hkv, T, bm = CONFIGS[args.config]
-    cache = build_cache(args.config, device, seed=1234 + rank, precision=args.precision)
+    _, Hq, Hkv, T, bm = CONFIGS[args.config]
+    B = local_batch(args.config, world)
+    cache = build_cache(args.config, device, seed=1234 + rank, precision=args.precision,
+                        world=world)
     gen = torch.Generator(device=device)
     gen.manual_seed(99 + rank)
     q = torch.randn(B, Hq, D, device=device, generator=gen)
     out = torch.empty(B, Hq, D, device=device)
-    # weak scaling: global batch B * world, each rank owns a contiguous batch
-    # range (paper_2505_18231_b200.sharding); one all-gather of outputs/step
-    from paper_2505_18231_b200.sharding import gather_outputs, plan_shards
+    # each rank owns a contiguous batch range (paper_2505_18231_b200.sharding);
+    # one all-gather of outputs per step into a pre-allocated buffer
+    from paper_2505_18231_b200.sharding import gather_buffer, gather_outputs, plan_shards
 
-    plan = plan_shards(B * world, Hkv, Hq, world, rank)
+    gb = B * world
+    plan = plan_shards(gb, Hkv, Hq, world, rank)
+    gbuf = gather_buffer(plan, out) if world > 1 else None
 
     def step():
         cache.attend(q, out=out)
         if world > 1:
-            gather_outputs(plan, out)
+            gather_outputs(plan, out, buf=gbuf)
 
     def barrier():
         if world > 1:
@@ -252,14 +300,8 @@ def run_ours(args) -> dict | None:
     sbytes = step_bytes(B, Hq, Hkv, T, bm)
     value = sbytes * world / (ms * 1e-3) / 1e9
 
-    # dominant kernel: time the attend launch alone (CUDA events on its stream)
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record()
-    for _ in range(args.steps):
-        cache.attend(q, out=out)
-    k1.record()
-    torch.cuda.synchronize()
-    k_ms = k0.elapsed_time(k1) / args.steps
+    # dominant kernel: the attend launch alone (CUDA events on its stream)
+    k_ms = time_attend(cache, q, out, args.steps)
 
     # e2e through the public API: every step uploads its q from pinned host
     # memory, runs PagedKvCache.attend (+ the output all-gather when sharded)
@@ -283,7 +325,7 @@ def run_ours(args) -> dict | None:
             main.wait_event(up[cur])
             cache.attend(q_dev[cur], out=out_dev[cur])
             if world > 1:
-                gather_outputs(plan, out_dev[cur])
+                gather_outputs(plan, out_dev[cur], buf=gbuf)
             done[cur].record(main)
             with torch.cuda.stream(side):
                 if i + 1 < n:
@@ -318,7 +360,7 @@ def run_ours(args) -> dict | None:
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(args.config)
+            traffic = json.loads(tp.read_text()).get(f"{args.config}:{cache.precision}")
         except Exception:
             traffic = None
     res = {
@@ -330,16 +372,14 @@ def run_ours(args) -> dict | None:
         "warmup": args.warmup,
         "ms_per_step": round(ms, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.config in STRONG else "weak",
         "vs_baseline": None,
         "dtype": "u8 pages / fp32 accumulate",
-        "data": "synthetic N(0,1) K/V encoded by the product; N(0,1) q",
-        "config": {"workload": f"{args.config}: batch {B}/rank, {Hq}q/{Hkv}kv heads, d128, "
-                               f"context {T}, {bm}-bit",
-                   "global_batch": B * world, "seq_len": T, "parallelism": f"batch-sharded x{world}",
-                   "precision": cache.precision,
+        "data": "synthetic N(0,1) K/V (bf16) encoded by the product; N(0,1) q",
+        "config": {**config_dict(args.config, world),
                    "l2": "inputs larger than L2 (packed cache %.0f MB/rank)" % (sbytes / 1e6)},
-        "tokens_per_s": round(B * world / (ms * 1e-3), 1),
+        "precision": cache.precision,
+        "tokens_per_s": round(gb / (ms * 1e-3), 1),
         "e2e": {"value": round(sbytes * world / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                 "h2d_bytes_per_step": B * Hq * D * 4, "d2h_bytes_per_step": B * Hq * D * 4,
                 "ms_per_step": round(e2e_ms, 4),
@@ -355,11 +395,86 @@ def run_ours(args) -> dict | None:
         "gpu_launches": int(launches),
     }
     if world == 1 and not args.no_extras:
+        extras = {}
+        if args.config == "c2":
+            # the like-for-like all-hi+lo mode on the same cache
+            prev = cache.precision
+            cache.precision = "precise"
+            extras["c2_precise"] = kernel_line(sbytes, time_attend(cache, q, out, args.steps), peak)
+            cache.precision = prev
         res["serving_step"] = measure_serving(cache, q, steps=2 * R)
-        res["encode"] = measure_encode(device, bm)
+        del cache
+        torch.cuda.empty_cache()
+        if args.config == "c2":
+            for name in ("c2_1b", "c4"):
+                extras[name] = measure_config(name, device, peak, steps=max(10, args.steps // 5))
+        res["extras"] = extras
+        res["encode"] = {f"{m}b": measure_encode(device, m) for m in (2, 1)}
+        res["parity"] = c1_parity()
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
     return res
+
+
+def kernel_line(sbytes: int, ms: float, peak: float) -> dict:
+    gbs = sbytes / (ms * 1e-3) / 1e9
+    return {"ms": round(ms, 4), "GBps": round(gbs, 1), "frac": round(gbs / peak, 4)}
+
+
+def measure_config(name: str, device, peak: float, steps: int) -> dict:
+    """One more BASELINE workload on this GPU (default precision)."""
+    import torch
+
+    _, Hq, Hkv, T, bm = CONFIGS[name]
+    B = local_batch(name, 1)
+    cache = build_cache(name, device, seed=4321)
+    q = torch.randn(B, Hq, D, device=device)
+    out = torch.empty(B, Hq, D, device=device)
+    sb = step_bytes(B, Hq, Hkv, T, bm)
+    line = kernel_line(sb, time_attend(cache, q, out, steps), peak)
+    line.update({"workload": config_dict(name, 1)["workload"], "precision": cache.precision,
+                 "tokens_per_s": round(B / (line["ms"] * 1e-3), 1)})
+    del cache
+    torch.cuda.empty_cache()
+    return line
+
+
+def c1_parity() -> dict:
+    """Counted differences of the GPU's pages against the REFERENCE's own
+    serialized chunks on BASELINE config 1 (tests/golden/c1_*.npz, made by
+    tests/golden/gen_c1.py), and the decode error against its outputs."""
+    import torch
+
+    import paper_2505_18231_b200 as P
+    from tests.golden.inputs import c1_inputs, c1_value_entries
+    from tests.parity_bounds import summarize
+    from tests.wirediff import compare
+
+    counts, worst = [], 0.0
+    for case in c1_inputs():
+        with np.load(ROOT / "tests" / "golden" / f"c1_{case['name']}.npz") as z:
+            g = {k: z[k] for k in ("k_wire", "v_wire", "out")}
+        cb_k = P.default_codebook(f"{case['bit_mode']}b")
+        cb_v = cb_k if not case["distinct_v"] else P.Codebook(
+            entries=c1_value_entries(cb_k.entries, True), bit_mode=cb_k.bit_mode)
+        H = case["keys"].shape[0]
+        c = P.PagedKvCache(P.CacheConfig(d=D, bit_mode=cb_k.bit_mode), 1, H, cb_k=cb_k, cb_v=cb_v)
+        k = torch.from_numpy(case["keys"][None]).cuda()
+        v = torch.from_numpy(case["values_ht"][None]).cuda()
+        for a, b in case["batches"]:
+            c.append(k[:, :, a:b], v[:, :, a:b])
+        for kind in ("k", "v"):
+            got = np.stack([c.wire_chunks(u, kind) for u in range(H)])
+            counts.append(compare(got, g[f"{kind}_wire"], case["bit_mode"]))
+        out = c.attend(torch.from_numpy(case["q"].reshape(1, -1, D)).cuda()).cpu().numpy()
+        out = out.reshape(g["out"].shape)
+        err = np.abs(out - g["out"]).max(axis=-1) / np.abs(g["out"]).max(axis=-1)
+        worst = max(worst, float(err.max()))
+    tot = summarize(counts)
+    tot["decode_max_rel_err"] = float(f"{worst:.3g}")
+    tot["what"] = ("BASELINE config 1 (8 KV heads x 4133 tokens, 1b/2b, N(0,1)/misaligned) vs the "
+                   "reference's serialized chunks and attend_quantized outputs")
+    return tot
 
 
 def measure_serving(cache, q, steps: int) -> dict:
@@ -440,12 +555,12 @@ def cpu_baseline(cfg_name: str, budget_s: float = 15.0, threads: int | None = No
     G q-heads of every unit, repeated until `budget_s` of CPU work."""
     from oracle import oracle as orc
 
-    import paper_2505_18231_b200 as P
-
     B, Hq, Hkv, T, bm = CONFIGS[cfg_name]
     G = Hq // Hkv
     cores = threads or os.cpu_count() or 1
-    cb = P.default_codebook(f"{bm}b")
+    # the shipped codebook read by the oracle's own NSNC reader: this arm
+    # never loads the product package or its CUDA library
+    ent, _ = orc.load_nsnc_entries(ROOT / "paper_2505_18231_b200" / "codebooks" / f"cb{bm}_seed0.nsnc")
     n_chunks = T // R
     key = (cfg_name, cores)
     if key not in _CPU_SAMPLE:
@@ -454,8 +569,8 @@ def cpu_baseline(cfg_name: str, budget_s: float = 15.0, threads: int | None = No
         g = np.random.Generator(np.random.PCG64(7))
         k = g.standard_normal((n_chunks, R, D), dtype=np.float32)
         v = g.standard_normal((n_chunks, R, D), dtype=np.float32)
-        kw = orc.encode_many(k, True, cb.entries, bm, threads=cores)  # keys at pos 0 per chunk
-        vw = orc.encode_many(v, False, cb.entries, bm, threads=cores)
+        kw = orc.encode_many(k, True, ent, bm, threads=cores)  # keys at pos 0 per chunk
+        vw = orc.encode_many(v, False, ent, bm, threads=cores)
         kws = np.ascontiguousarray(np.broadcast_to(kw.reshape(1, -1), (cores, kw.size)))
         vws = np.ascontiguousarray(np.broadcast_to(vw.reshape(1, -1), (cores, vw.size)))
         q = g.standard_normal((cores, G, D), dtype=np.float32)
@@ -464,7 +579,7 @@ def cpu_baseline(cfg_name: str, budget_s: float = 15.0, threads: int | None = No
     n_units = cores
     reps, t0 = 0, time.perf_counter()
     while True:
-        orc.attend_many(kws, vws, n_units, n_chunks, cb.entries, cb.entries, bm, q, threads=cores)
+        orc.attend_many(kws, vws, n_units, n_chunks, ent, ent, bm, q, threads=cores)
         reps += 1
         dt = time.perf_counter() - t0
         if dt >= budget_s:
@@ -473,7 +588,10 @@ def cpu_baseline(cfg_name: str, budget_s: float = 15.0, threads: int | None = No
     return {"value": round(reps * n_units * unit_bytes / dt / 1e9, 4), "unit": "GB/s", "cores": cores,
             "kind": "port",
             "sample": f"{reps} x {n_units} full-context units x {G} q-heads ({T} tokens, {bm}-bit) "
-                      f"decoded in {dt:.2f}s on {cores} threads (one decode per unit per repetition)",
+                      f"decoded in {dt:.2f}s on {cores} threads; extrapolated to the workload "
+                      f"({B * Hkv} units per rank): the per-unit decode cost is data-independent, "
+                      f"so GB/s does not depend on the unit count",
+            "extrapolated": True,
             "seconds": round(dt, 3)}
 
 
@@ -482,7 +600,6 @@ def run_reference(args) -> dict | None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    B, Hq, Hkv, T, bm = CONFIGS[args.config]
     vals = []
     # seconds of CPU work per step: 3 s, less when many steps are asked for so
     # the whole run stays within ~2.5 minutes
@@ -497,10 +614,9 @@ def run_reference(args) -> dict | None:
     return {
         "impl": "reference", "metric": "packed-KV decode attention GB/s", "value": value,
         "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8 pages / fp32 accumulate", "data": "synthetic N(0,1)",
-        "config": {"workload": f"{args.config}: batch {B}, {Hq}q/{Hkv}kv heads, d128, "
-                               f"context {T}, {bm}-bit", "global_batch": B, "seq_len": T},
+        "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak",
+        "vs_baseline": None, "dtype": "u8 pages / fp32 accumulate", "data": "synthetic N(0,1)",
+        "config": config_dict(args.config, world),
         "cpu_baseline": {**best, "value": value},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -517,11 +633,22 @@ def main():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the serving-step and encode measurements")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--precision", default=None, choices=["precise", "balanced", "fast"],
+    ap.add_argument("--precision", default=None, choices=["precise", "vfast"],
                     help="decode codeword precision (DESIGN.md 3.2); default: the library's "
-                         "(fast for 2-bit, precise for 1-bit)")
+                         "(vfast for 2-bit, precise for 1-bit)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+               str(Path(__file__).resolve()), *sys.argv[1:]]
+        raise SystemExit(subprocess.run(cmd).returncode)
     res = run_reference(args) if args.impl == "reference" else run_ours(args)
     if res is not None:
         print(json.dumps(res), flush=True)

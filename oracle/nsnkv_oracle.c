@@ -508,7 +508,7 @@ typedef struct {
   int64_t begin, end;
   /* encode */
   const float *rows; int is_key; const float *rope_cs; const float *entries; const double *inv;
-  int bit_mode, strategy; uint8_t *wire;
+  int bit_mode, strategy; uint8_t *wire; const int64_t *pos0;
   /* attend */
   const uint8_t *kw, *vw; int n_chunks; const float *ent_k, *ent_v; const float *q; int G;
   float *out; int64_t units_stride_k;
@@ -519,7 +519,8 @@ static void *worker(void *arg) {
   int wb = orc_wire_bytes(j->bit_mode);
   for (int64_t i = j->begin; i < j->end; ++i) {
     if (j->kind == 0) {
-      orc_encode_chunk(j->rows + i * R * D, j->is_key, j->rope_cs, j->entries, j->inv,
+      const float *cs = j->rope_cs && j->pos0 ? j->rope_cs + j->pos0[i] * (2 * NPAIR) : j->rope_cs;
+      orc_encode_chunk(j->rows + i * R * D, j->is_key, cs, j->entries, j->inv,
                        j->bit_mode, j->strategy, j->wire + i * wb, NULL, NULL);
     } else {
       orc_attend(j->kw + i * j->units_stride_k, j->vw + i * j->units_stride_k, j->n_chunks, NULL,
@@ -553,6 +554,18 @@ void orc_encode_many(const float *rows, int64_t n, int is_key, const float *rope
   memset(&p, 0, sizeof(p));
   p.kind = 0; p.rows = rows; p.is_key = is_key; p.rope_cs = rope_cs; p.entries = entries;
   p.inv = inv; p.bit_mode = bit_mode; p.strategy = strategy; p.wire = wire;
+  run_jobs(&p, n, threads);
+}
+
+/* n chunks of [64][128] rows; chunk i's first position is row pos0[i] of the
+ * rope table (keys), so whole caches encode in one call (parity tests) */
+void orc_encode_many_pos(const float *rows, int64_t n, int is_key, const float *rope_table,
+                         const int64_t *pos0, const float *entries, const double *inv,
+                         int bit_mode, int strategy, uint8_t *wire, int threads) {
+  job_t p;
+  memset(&p, 0, sizeof(p));
+  p.kind = 0; p.rows = rows; p.is_key = is_key; p.rope_cs = rope_table; p.pos0 = pos0;
+  p.entries = entries; p.inv = inv; p.bit_mode = bit_mode; p.strategy = strategy; p.wire = wire;
   run_jobs(&p, n, threads);
 }
 

@@ -49,6 +49,7 @@ def lib():
         L.orc_attend.argtypes = [P, P, i32, P, P, i32, i64, P, P, P, i32, P, i32, P, P, P]
         L.orc_encode_many.argtypes = [P, i64, i32, P, P, P, i32, i32, P, i32]
         L.orc_attend_many.argtypes = [P, P, i64, i32, P, P, P, i32, P, i32, P, i32]
+        L.orc_encode_many_pos.argtypes = [P, i64, i32, P, P, P, P, i32, i32, P, i32]
         L.orc_f32_to_f16.argtypes = [ctypes.c_float]
         L.orc_f32_to_f16.restype = ctypes.c_uint16
         _lib = L
@@ -218,6 +219,23 @@ def encode_many(rows: np.ndarray, is_key: bool, entries, bit_mode: int, strategy
     return wire
 
 
+def encode_many_pos(rows: np.ndarray, is_key: bool, pos0: np.ndarray, entries, bit_mode: int,
+                    strategy: int = 3, rope_base: float = 10000.0,
+                    threads: int | None = None) -> np.ndarray:
+    """n chunks [n, 64, 128]; chunk i starts at absolute position pos0[i]
+    (keys are rotated there, kvcache.py:114-136) -> wire chunks [n, W]."""
+    x = np.ascontiguousarray(rows, np.float32)
+    n = x.shape[0]
+    e = np.ascontiguousarray(entries, np.float32)
+    inv = entry_inv_norms(e)
+    p0 = np.ascontiguousarray(pos0, np.int64)
+    cs = rope_table(int(p0.max()) + R, rope_base) if is_key and n else None
+    wire = np.empty((n, wire_bytes(bit_mode)), np.uint8)
+    lib().orc_encode_many_pos(_p(x), n, int(bool(is_key)), _p(cs), _p(p0), _p(e), _p(inv),
+                              int(bit_mode), int(strategy), _p(wire), threads or os.cpu_count() or 1)
+    return wire
+
+
 def attend_many(kw: np.ndarray, vw: np.ndarray, n_units: int, n_chunks: int, ent_k, ent_v,
                 bit_mode: int, q: np.ndarray, threads: int | None = None) -> np.ndarray:
     """CPU baseline: n_units units of n_chunks wire chunks, G queries each."""
@@ -230,3 +248,31 @@ def attend_many(kw: np.ndarray, vw: np.ndarray, n_units: int, n_chunks: int, ent
                           _p(np.ascontiguousarray(ent_v, np.float32)), int(bit_mode), _p(qq), G,
                           _p(out), threads or os.cpu_count() or 1)
     return out
+
+
+# -- codebook.py:384-432 (NSNC file) ------------------------------------------
+def load_nsnc_entries(path) -> tuple[np.ndarray, int]:
+    """(active entries [256, 8] float32, bit mode) of an NSNC codebook file,
+    read without the product package (the bench's reference arm must not load
+    it).  Layout: b"NSNC", <u16 version, u8 bit mode, u64 seed, u8 tuned>,
+    256x8 <f4 entries, u8 packed4 flag [, <f4 scale, 1024 nibble bytes]>.
+    With a packed4 block the active entries are its dequantized levels
+    (codebook.py:57-68)."""
+    import struct
+
+    data = Path(path).read_bytes()
+    if data[:4] != b"NSNC":
+        raise ValueError("not an NSNC codebook")
+    version, mode, _seed, _tuned = struct.unpack_from("<HBQB", data, 4)
+    pos = 4 + 12
+    e = np.frombuffer(data, "<f4", 2048, pos).reshape(256, 8).astype(np.float32)
+    pos += 8192
+    if data[pos]:
+        (scale,) = struct.unpack_from("<f", data, pos + 1)
+        b = np.frombuffer(data, np.uint8, 1024, pos + 5)
+        lv = np.empty(2048, np.float32)
+        lv[0::2] = b & 15
+        lv[1::2] = b >> 4
+        lv = lv.reshape(256, 8)
+        e = lv * np.float32(scale) if mode == 2 else (lv - np.float32(7.5)) * np.float32(scale)
+    return np.ascontiguousarray(e, np.float32), int(mode)

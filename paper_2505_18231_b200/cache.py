@@ -40,15 +40,34 @@ NPAIR = D // 2
 PAGE_BYTES = {BitMode.TWO_BIT: 2304, BitMode.ONE_BIT: 1280}
 LEDGER_BYTES = {BitMode.TWO_BIT: 2292, BitMode.ONE_BIT: 1268}
 CNT_CLAMP, CNT_ZERO, CNT_FALLBACK, CNT_NEARTIE = range(4)
-PRECISIONS = {"precise": 0, "balanced": 1, "fast": 2}
+# decode codeword precision (C-ABI nsnkv_cache_view.precision)
+PRECISIONS = {"precise": 0, "vfast": 1, "fast": 2}
 
 
 def default_precision(bit_mode) -> str:
-    """2-bit: plain fp16 codewords ("fast"; the random per-component signs
-    keep the rounding unbiased, every parity case stays within the 1e-3
-    output tolerance); 1-bit: fp16 hi + lo codewords ("precise"; plain fp16
-    misses the tolerance on the misaligned fixture)."""
-    return "fast" if int(bit_mode) == 2 else "precise"
+    """Key codewords always enter the score product as fp16 hi + lo: a plain
+    fp16 key codeword (11-bit significand) puts a relative error of ~2^-12 on
+    every score, and with large-magnitude scores (outlier tokens) that shifts
+    the softmax far beyond the 1e-3 output tolerance (2-bit misaligned data,
+    4K context: 3e-2).  Value codewords may be plain fp16 in
+    2-bit mode ("vfast": the per-component signs make the rounding errors
+    cancel, <= 2.5e-4 at 32K context), but not in 1-bit mode, where the
+    unsigned codewords accumulate a bias that grows with the context (1.5e-3
+    at 4K, 3.7e-3 at 32K), so 1-bit decodes "precise"."""
+    return "vfast" if int(bit_mode) == 2 else "precise"
+
+
+def check_precision(precision: str, bit_mode, allow_inexact: bool = False) -> str:
+    """Validate a precision mode for a bit mode.  Modes that are known to
+    exceed the 1e-3 output tolerance on some inputs ("fast" in either bit
+    mode, "vfast" in 1-bit mode) need an explicit allow_inexact=True."""
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
+    inexact = precision == "fast" or (precision == "vfast" and int(bit_mode) == 1)
+    if inexact and not allow_inexact:
+        raise Unsupported(f"precision {precision!r} exceeds the 1e-3 output tolerance on some "
+                          f"{int(bit_mode)}-bit inputs; pass allow_inexact=True to use it")
+    return precision
 
 
 class ScaleStrategy(enum.IntEnum):
@@ -140,6 +159,16 @@ class RopeTable:
         return self.cs
 
 
+def resolve_device(device=None) -> torch.device:
+    """An indexed CUDA device: None or "cuda" without an index means the
+    calling thread's current device (one process per GPU after
+    torch.cuda.set_device(rank)), never GPU 0."""
+    d = torch.device("cuda") if device is None else torch.device(device)
+    if d.type != "cuda":
+        raise Unsupported(f"the packed cache lives on a CUDA device, got {d}")
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -153,25 +182,24 @@ class PagedKvCache:
     def __init__(self, config: CacheConfig, batch: int, n_kv_heads: int, max_tokens: int = 0,
                  cb_k: Codebook | None = None, cb_v: Codebook | None = None,
                  base_position: int = 0, device=None, check_finite: bool = True,
-                 precision: str | None = None):
+                 precision: str | None = None, allow_inexact: bool = False):
         config.check_gpu_path()
         if precision is None:  # deployment default; NSNKV_PRECISION overrides
             precision = os.environ.get("NSNKV_PRECISION") or default_precision(config.bit_mode)
+        # check_finite mirrors the reference's as_tensor2d validation
+        # (core.py:38); it costs one device->host sync per append, so a server
+        # that validates its activations elsewhere passes False
         self.check_finite = check_finite
-        # decode codeword precision: "precise" = fp16 hi + lo
-        # on both sides, "balanced" = plain fp16 scores / hi + lo values,
-        # "fast" = plain fp16 both (2-bit only)
-        if precision not in PRECISIONS:
-            raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
-        self.precision = precision
+        self.precision = check_precision(precision, config.bit_mode, allow_inexact)
         if batch < 1 or n_kv_heads < 1:
             raise ShapeMismatch("batch and n_kv_heads must be >= 1")
+        if int(base_position) < 0:
+            raise Unsupported("base_position must be >= 0 (the RoPE table starts at position 0)")
         self.config = config
         self.batch = batch
         self.n_kv_heads = n_kv_heads
         self.units = batch * n_kv_heads
-        self.device = torch.device(device) if device is not None else torch.device(
-            "cuda", torch.cuda.current_device())
+        self.device = resolve_device(device)
         self.bit_mode = config.bit_mode
         self.page_bytes = PAGE_BYTES[self.bit_mode]
         self.cb_k = cb_k
@@ -253,6 +281,8 @@ class PagedKvCache:
         v = self._as_rows(values)
         if k.shape != v.shape:
             raise ShapeMismatch("key and value batches must have the same shape")
+        if k.dtype != v.dtype:  # one fp32 / one bf16 batch: encode both from fp32
+            k, v = k.float(), v.float()
         n = k.shape[1]
         if n < 1:
             raise ShapeMismatch("append needs at least one token")
@@ -262,7 +292,6 @@ class PagedKvCache:
             start = self.base_position + self.n_chunks * R
             table = self.rope.ensure(start + n_flush * R)
             page_ids = self.page_table[:, self.n_chunks:]
-            bf16 = 1 if k.dtype == torch.bfloat16 else 0
             start_t = self._start_pos(start)
             for is_key, rows, res, pool, cb, cnt in (
                     (1, k, self.k_res, self.k_pool, cb_k, self.k_counters),
@@ -270,7 +299,8 @@ class PagedKvCache:
                 cnt_view = cnt[:, self.n_chunks:self.n_chunks + n_flush]
                 cnt_buf = torch.empty(self.units, n_flush, 4, dtype=torch.int32, device=self.device)
                 _lib.check(_lib.lib.nsnkv_encode_chunks(
-                    res.data_ptr(), self.n_res, rows.data_ptr(), bf16, n, self.units, n_flush,
+                    res.data_ptr(), self.n_res, rows.data_ptr(),
+                    1 if rows.dtype == torch.bfloat16 else 0, n, self.units, n_flush,
                     is_key, start_t.data_ptr(),
                     table.data_ptr(), 0, table.shape[0], cb.device_handle(self.device),
                     int(self.config.strategy), pool.data_ptr(), page_ids.data_ptr(),
@@ -397,8 +427,17 @@ class PagedKvCache:
         if self.total_tokens == 0:
             raise ShapeMismatch("attention over an empty cache")
         cv = self.view(q.shape[1])
+        rows = self.batch * q.shape[1]
         if out is None:
             out = torch.empty(self.batch, q.shape[1], D, dtype=torch.float32, device=self.device)
+        # the kernels write fp32 [B*Hq, 128] / [B*Hq] through raw pointers
+        for name, t, n in (("out", out, rows * D), ("lse", lse, rows)):
+            if t is None:
+                continue
+            if (t.dtype != torch.float32 or not t.is_contiguous() or t.device != self.device
+                    or t.numel() != n):
+                raise ShapeMismatch(f"{name} must be a contiguous float32 tensor of {n} elements "
+                                    f"on {self.device}, got {t.dtype} {tuple(t.shape)} on {t.device}")
         ws = self._workspace(cv)
         _lib.check(_lib.lib.nsnkv_decode_attend(cv, q.data_ptr(), out.data_ptr(),
                                                 lse.data_ptr() if lse is not None else None,
@@ -418,8 +457,12 @@ class PagedKvCache:
         ids = self.page_table[unit, :self.n_chunks].long()
         return pool[ids].cpu().numpy()
 
+    def wire_chunks(self, unit: int, kind: str = "k") -> np.ndarray:
+        """[n_chunks, wire_bytes] reference serialized chunks of one unit."""
+        return pages_to_wire(self.pages(unit, kind), self.bit_mode, self.config.strategy)
+
     def chunk_wire(self, unit: int, kind: str = "k") -> list[bytes]:
-        return [page_to_wire(p, self.bit_mode, self.config.strategy) for p in self.pages(unit, kind)]
+        return [w.tobytes() for w in self.wire_chunks(unit, kind)]
 
     def snapshot(self, unit: int = 0) -> bytes:
         """kvcache.snapshot byte image of one unit (kvcache.py:198-213)."""
@@ -445,46 +488,69 @@ _LAYOUT = {  # idx, sgn, s2, s1n, on, par
 
 
 def unpermute_signs(words: np.ndarray) -> np.ndarray:
-    """[64, 4] u32 decode-order sign words -> natural sign bytes [64, 16].
+    """[..., 64, 4] u32 decode-order sign words -> natural sign bytes [..., 64, 16].
     Word q of a token covers subs 4q+m; bit 4m+p holds the sign of component
     2p and bit 16+4m+p the sign of component 2p+1 (see csrc/common.cuh)."""
     w = words.astype(np.uint32)
-    out = np.zeros((w.shape[0], 16), np.uint32)
+    out = np.zeros(w.shape[:-1] + (16,), np.uint32)
     for q in range(4):
         for m in range(4):
             for p in range(4):
-                out[:, 4 * q + m] |= ((w[:, q] >> (4 * m + p)) & 1) << (2 * p)
-                out[:, 4 * q + m] |= ((w[:, q] >> (16 + 4 * m + p)) & 1) << (2 * p + 1)
+                out[..., 4 * q + m] |= ((w[..., q] >> (4 * m + p)) & 1) << (2 * p)
+                out[..., 4 * q + m] |= ((w[..., q] >> (16 + 4 * m + p)) & 1) << (2 * p + 1)
     return out.astype(np.uint8)
 
 
 def permute_signs(signs: np.ndarray) -> np.ndarray:
-    """Natural sign bytes [64, 16] -> decode-order words [64, 4] u32."""
+    """Natural sign bytes [..., 64, 16] -> decode-order words [..., 64, 4] u32."""
     s = signs.astype(np.uint32)
-    words = np.zeros((s.shape[0], 4), np.uint32)
+    words = np.zeros(s.shape[:-1] + (4,), np.uint32)
     for q in range(4):
         for m in range(4):
             for p in range(4):
-                words[:, q] |= ((s[:, 4 * q + m] >> (2 * p)) & 1) << (4 * m + p)
-                words[:, q] |= ((s[:, 4 * q + m] >> (2 * p + 1)) & 1) << (16 + 4 * m + p)
+                words[..., q] |= ((s[..., 4 * q + m] >> (2 * p)) & 1) << (4 * m + p)
+                words[..., q] |= ((s[..., 4 * q + m] >> (2 * p + 1)) & 1) << (16 + 4 * m + p)
     return words
 
 
-def page_to_wire(page: np.ndarray, bit_mode: BitMode, strategy: ScaleStrategy) -> bytes:
+def wire_bytes(bit_mode) -> int:
+    """Bytes of one serialized chunk (vq.py:363-380)."""
+    return 6 + 1024 + (1024 if int(bit_mode) == 2 else 0) + 36 + 80 + 128
+
+
+def pages_to_wire(pages: np.ndarray, bit_mode, strategy) -> np.ndarray:
+    """[n, page_bytes] device pages -> [n, wire_bytes] reference serialized
+    chunks (vq.py:363-380), vectorised over chunks."""
     bm = BitMode(bit_mode)
     o_idx, o_sgn, o_s2, o_s1n, o_on, o_par = _LAYOUT[bm]
-    p = np.asarray(page, dtype=np.uint8)
-    par = p[o_par:o_par + 20].view("<u2")
-    out = bytearray(struct.pack("<HHBB", R, D, int(bm), int(strategy)))
-    out += p[o_idx:o_idx + 1024].tobytes()
+    p = np.ascontiguousarray(pages, dtype=np.uint8).reshape(-1, PAGE_BYTES[bm])
+    n = p.shape[0]
+    out = np.empty((n, wire_bytes(bm)), np.uint8)
+    out[:, :6] = np.frombuffer(struct.pack("<HHBB", R, D, int(bm), int(strategy)), np.uint8)
+    pos = 6
+    out[:, pos:pos + 1024] = p[:, o_idx:o_idx + 1024]
+    pos += 1024
     if bm is BitMode.TWO_BIT:
-        out += unpermute_signs(p[o_sgn:o_sgn + 1024].view("<u4").reshape(R, 4)).tobytes()
-    out += struct.pack("<HH", int(par[0]), int(par[1])) + p[o_s1n:o_s1n + 32].tobytes()
-    for g in range(4):
-        out += struct.pack("<HH", int(par[2 + g]), int(par[6 + g]))
-    out += p[o_on:o_on + 64].tobytes()
-    out += p[o_s2:o_s2 + 128].tobytes()
-    return bytes(out)
+        w = p[:, o_sgn:o_sgn + 1024].copy().view("<u4").reshape(n, R, 4)
+        out[:, pos:pos + 1024] = unpermute_signs(w).reshape(n, 1024)
+        pos += 1024
+    par = p[:, o_par:o_par + 20]
+    out[:, pos:pos + 4] = par[:, 0:4]                       # s1 scale, zero
+    pos += 4
+    out[:, pos:pos + 32] = p[:, o_s1n:o_s1n + 32]
+    pos += 32
+    for g in range(4):                                      # (o scale, o zero) per group
+        out[:, pos:pos + 2] = par[:, 4 + 2 * g:6 + 2 * g]
+        out[:, pos + 2:pos + 4] = par[:, 12 + 2 * g:14 + 2 * g]
+        pos += 4
+    out[:, pos:pos + 64] = p[:, o_on:o_on + 64]
+    pos += 64
+    out[:, pos:pos + 128] = p[:, o_s2:o_s2 + 128]
+    return out
+
+
+def page_to_wire(page: np.ndarray, bit_mode: BitMode, strategy: ScaleStrategy) -> bytes:
+    return pages_to_wire(np.asarray(page)[None], bit_mode, strategy)[0].tobytes()
 
 
 def wire_to_page(blob: bytes) -> np.ndarray:

@@ -116,8 +116,9 @@ class Codebook:
 
         from ._lib import c_void_p, check, lib
 
-        dev = torch.device("cuda", torch.cuda.current_device() if device is None
-                           else torch.device(device).index or 0)
+        from .cache import resolve_device
+
+        dev = resolve_device(device)
         key = dev.index
         h = self._handles.get(key)
         if h is None:

@@ -74,6 +74,20 @@ __device__ __forceinline__ uint16_t f32_to_f16_bits(float x) {
   return __half_as_ushort(__float2half_rn(x));
 }
 
+// Set a kernel's dynamic shared-memory attributes once per DEVICE (not once
+// per process: a process driving two GPUs must set it on each).  `done` is a
+// per-kernel bitmask of device ordinals.
+template <typename K>
+inline void set_smem_attr_once(K kern, int bytes, unsigned long long &done, int carveout = -1) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (carveout >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  __atomic_fetch_or(&done, bit, __ATOMIC_ACQ_REL);
+}
+
 }  // namespace nsnkv
 
 // Launch bookkeeping shared by all translation units (capi.cu owns it).

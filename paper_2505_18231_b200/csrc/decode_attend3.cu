@@ -39,23 +39,6 @@
 
 namespace nsnkv {
 
-#ifdef NSNKV_TRACE
-// debug timeline of CTA 0 (built only into the trace library): per warp,
-// 4096 records of clock64 << 24 | event << 16 | item, plain stores
-__device__ unsigned long long g_trace[16][4096];
-#define A3_TRACE(role, ev, item)                                                          \
-  do {                                                                                   \
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && tr_i < 4096u)                      \
-      g_trace[threadIdx.x >> 5][tr_i++] =                                                \
-          ((unsigned long long)clock64() << 24) | ((unsigned long long)(ev) << 16) | (unsigned)(item); \
-  } while (0)
-#define A3_TRACE_DECL unsigned tr_i = 0
-#else
-#define A3_TRACE(role, ev, item) \
-  do {                           \
-  } while (0)
-#define A3_TRACE_DECL
-#endif
 
 template <int G, bool FOLD, int PREC>
 struct A3 {
@@ -73,13 +56,7 @@ struct A3 {
   static constexpr int TAILS = CP * 2 * META;  // producer's staged page tails per item
   static constexpr bool ONE_TABLE = PREC == 2;     // K hi | V hi interleaved per entry
   static constexpr int TBL = ONE_TABLE ? 65536 : 131072;
-#ifndef NSNKV_FULL_SLEEP_NS
-#define NSNKV_FULL_SLEEP_NS 128  // consumer poll interval while its page payload is in flight
-#endif
-#ifndef NSNKV_FAST_BATCH
-#define NSNKV_FAST_BATCH 2
-#endif
-  static constexpr int FB = ONE_TABLE ? NSNKV_FAST_BATCH : 1;
+  static constexpr int FB = ONE_TABLE ? 2 : 1;    // items per shift-term MMA chain
   static constexpr int ZB = 4096 * FB;             // B operand: K 128 x N fp16
   static constexpr int NSLOT = ONE_TABLE ? (FB == 2 ? 4 : 3) : 2;  // producer -> consumer item slots
   static constexpr int NZB = 1;                    // shift-term B operand buffers per group
@@ -202,35 +179,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
   return ok != 0;
 }
 
-// producer-side wait: back off with nanosleep so a waiting producer does not
-// take issue slots from the consumer warps of its SM sub-partition
-// producer / stream waits: a try_wait loop (hardware-suspended); the
-// nanosleep back-off of earlier kernels is kept behind -DNSNKV_WAIT_SLEEP_POLL
-// (measured 0.2-0.5 % slower now that no waiter spins)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-#ifndef NSNKV_WAIT_SLEEP_POLL
-  mbar_wait(bar, parity);
-  return;
-#endif
-  const uint32_t a = smem_u32(bar);
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(a), "r"(parity)
-      : "memory");
-  while (!ok) {
-    __nanosleep(64);
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-
 // rtn4_dequant (vq.py:133-136): zero + level * scale, two fp32 roundings
 __device__ __forceinline__ float rtn4(uint32_t level, float zero, float scale) {
   return __fadd_rn(zero, __fmul_rn((float)level, scale));
@@ -242,14 +190,13 @@ __global__ void __launch_bounds__(512, 1)
                    int64_t total_chunks) {
   using C = A3<G, FOLD, PREC>;
   constexpr int CP = C::CP, NTP = C::NTP, NGRP = C::NGRP, NSTAGE = C::NSTAGE;
-  constexpr bool HILO_K = PREC == 0;
-  constexpr bool HILO_V = PREC <= 1;
+  constexpr bool HILO_K = PREC <= 1;  // precise (0) and vfast (1): fp16 hi + lo key codewords
+  constexpr bool HILO_V = PREC == 0;  // precise only: fp16 hi + lo value codewords
   constexpr PageLayout L = page_layout(FOLD ? 2 : 1);
   constexpr uint32_t PB = (uint32_t)C::PAGE;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_units = cv.batch * cv.n_kv_heads;
-  A3_TRACE_DECL;
 
   const int grid = gridDim.x;
   const int64_t lo = range_lo(total_chunks, blockIdx.x, grid);
@@ -377,7 +324,7 @@ __global__ void __launch_bounds__(512, 1)
             }
             pg[q] = (int64_t)__shfl_sync(0xffffffffu, wv, c - wc0);
           }
-          if (nk >= C::NS) mbar_wait_sleep(&BR.empty[s2], (uint32_t)((nk / C::NS) - 1) & 1u);
+          if (nk >= C::NS) mbar_wait(&BR.empty[s2], (uint32_t)((nk / C::NS) - 1) & 1u);
           if (lane == 0) {
             uint8_t *st2 = ring + s2 * C::STAGE;
             mbar_expect_tx(&BR.full[s2], (uint32_t)cnt2 * 2u * MB);
@@ -387,7 +334,6 @@ __global__ void __launch_bounds__(512, 1)
             }
           }
           __syncwarp();
-          A3_TRACE(12, 0, k);
           item3_next<CP>(tit, hi, cv.n_chunks, n_units);
         }
       }
@@ -487,24 +433,18 @@ __global__ void __launch_bounds__(512, 1)
         rope_rows_p(nx, bp1, rcs_next);
         uint4 tl2[2];  // two items ahead: its page tails
         tail_load_p(it2, pid2, tl2);
-        A3_TRACE(warp, 0, n);
-        if (n >= NSLOT) mbar_wait_sleep(&BR.free_[gp][slot], (uint32_t)((n / NSLOT) - 1) & 1u);
-        A3_TRACE(warp, 1, n);
+        if (n >= NSLOT) mbar_wait(&BR.free_[gp][slot], (uint32_t)((n / NSLOT) - 1) & 1u);
         // stage the item's page tails; field offsets are relative to the tail
         __syncwarp();
         *reinterpret_cast<uint4 *>(P.tails + 32 * lane) = tl0[0];
         *reinterpret_cast<uint4 *>(P.tails + 32 * lane + 16) = tl0[1];
         __syncwarp();
-        A3_TRACE(warp, 2, n);
         const uint8_t *st = P.tails;
         // tail field offsets (the page layout's minus the payload size)
         constexpr PageLayout LT{L.idx, L.sgn, L.s2 - C::MAIN, L.s1n - C::MAIN, L.on - C::MAIN,
                                 L.par - C::MAIN, L.ledger - C::MAIN, L.bytes - C::MAIN};
         constexpr uint32_t TP = 2u * C::META;  // chunk stride in the staged tails
         typename C::Slot &SL = P.slot[slot];
-#ifdef NSNKV_DEBUG_SKIP_PRODUCE  // consumer-ceiling experiment: no producer work (wrong results)
-        if (false)
-#endif
         {
         // token scales (rtn4 s1, f16 s2) of tokens 2 lane, 2 lane + 1, keys and values
 #pragma unroll
@@ -539,24 +479,19 @@ __global__ void __launch_bounds__(512, 1)
           *reinterpret_cast<float4 *>(&SL.ov[c][4 * lane]) = o4;
         }
         }
-        A3_TRACE(warp, 3, n);
         // the MMA chain that last used this Z buffer (batch m - NZB) is done
         constexpr int BATCH = C::BATCH, NB = C::NB;
         const int m = n / BATCH, e = n % BATCH;
         if (m >= NZB) {
           const int n0 = (m - NZB) * BATCH;
-          mbar_wait_sleep(&BR.ready[gp][n0 % NSLOT], (uint32_t)((n0 / NSLOT) & 1));
+          mbar_wait(&BR.ready[gp][n0 % NSLOT], (uint32_t)((n0 / NSLOT) & 1));
         }
-        A3_TRACE(warp, 4, n);
         const uint32_t zb_s = smem_u32(P.zb[m % NZB]);
         // Z (MN-major B operand): element (k, n) at (k/8)*256 + (n/8)*128 +
         // (k%8)*16 + (n%8)*2 with k = 2j (cos coefficient a_j) / 2j + 1 (sin
         // coefficient b_j) and n = 8 (chunk | head group) + 2 head + (hi | lo):
         // each (j, chunk) writes two 16-byte rows (a_j and b_j for 4 heads x hi/lo);
         // lanes 4..7 of every 8 store the b row first (conflict-free phases)
-#if defined(NSNKV_DEBUG_SKIP_Z) || defined(NSNKV_DEBUG_SKIP_PRODUCE)  // ceiling experiments (wrong results)
-        if (false)
-#endif
 #pragma unroll
         for (int c = 0; c < CP; ++c) {
           float osc = 0.f, oz = 0.f, osc2 = 0.f, oz2 = 0.f;
@@ -617,7 +552,6 @@ __global__ void __launch_bounds__(512, 1)
         const bool issue = e == BATCH - 1 || nx.x >= hi;
         if (issue) tc05::fence_proxy_async();
         __syncwarp();
-        A3_TRACE(warp, 5, n);
         mbar_arrive(&BR.ready[gp][slot]);  // every lane: its scales and value shift vectors
         if (lane == 0) {
           if (issue) {  // issue the batch's shift-term MMA chain
@@ -625,9 +559,6 @@ __global__ void __launch_bounds__(512, 1)
             const int nf = m * BATCH;          // first item of the batch
             const uint32_t dcol = tmem + C::D_COL0 + (uint32_t)(16 * (NSLOT * gp + nf % NSLOT));
             constexpr uint32_t idesc = tc05::idesc_f16(128, NB) | (1u << 16);  // B MN-major
-#ifdef NSNKV_DEBUG_SKIP_PRODUCE
-            if (false)
-#endif
 #pragma unroll
             for (int kt = 0; kt < 8; ++kt)
               tc05::mma_f16_ts(dcol, tmem + 8 * kt,
@@ -637,7 +568,6 @@ __global__ void __launch_bounds__(512, 1)
           }
         }
         __syncwarp();
-        A3_TRACE(warp, 6, n);
         it = nx;
         it1 = it2;
         it2 = it3;
@@ -829,29 +759,9 @@ __global__ void __launch_bounds__(512, 1)
       }
       const int cnt = item3_count<CP>(cur);
       const int s = grp * C::NS + n % C::NS, slot = n % C::NSLOT;
-      A3_TRACE(warp, 0, n);
-      // page data: mbarrier try_wait (the warp is suspended in hardware until
-      // the phase completes or the time hint expires); measured 1-2 % faster
-      // than polling with nanosleep back-off (-DNSNKV_FULL_SLEEP_POLL)
-#ifndef NSNKV_FULL_SLEEP_POLL
       mbar_wait(&BR.full[s], (uint32_t)(n / C::NS) & 1u);
-#else
-      if (!mbar_test(&BR.full[s], (uint32_t)(n / C::NS) & 1u)) {
-        do {
-          __nanosleep(NSNKV_FULL_SLEEP_NS);
-        } while (!mbar_test(&BR.full[s], (uint32_t)(n / C::NS) & 1u));
-      }
-#endif
-      A3_TRACE(warp, 1, n);
       const uint8_t *st = ring + s * C::STAGE;
 
-#ifdef NSNKV_DEBUG_SKIP_CONSUME
-      // pipeline-ceiling experiment: wait for the producer slot, skip all math
-#ifndef NSNKV_DEBUG_SKIP_READY
-      mbar_wait(&BR.ready[grp][slot], (uint32_t)(n / C::NSLOT) & 1u);
-#endif
-      if (false) {
-#endif
       // ---- K side: payload dot products on tensor cores ----------------------
       const int tok0 = 16 * ws + g, tok1 = tok0 + 8;
       float pd[CP][NTP][2];
@@ -920,11 +830,7 @@ __global__ void __launch_bounds__(512, 1)
       }
 
       // ---- shift term (tensor memory) and token scales from the producer -----
-      A3_TRACE(warp, 2, n);
-#ifndef NSNKV_TRACE_NOREADY
       mbar_wait(&BR.ready[grp][slot], (uint32_t)(n / C::NSLOT) & 1u);
-#endif
-      A3_TRACE(warp, 3, n);
       tc05::fence_after();
       const typename C::Slot &SL = P.slot[slot];
       float sh[CP][NTP][2];
@@ -1014,9 +920,6 @@ __global__ void __launch_bounds__(512, 1)
 
       // ---- V side: accumulate P' . codewords on tensor cores -----------------
       const int vt0 = 16 * ws + 2 * t;
-#ifdef NSNKV_DEBUG_SKIP_VSIDE  // cost-split experiment: no value side (wrong results)
-      if (false)
-#endif
 #pragma unroll
       for (int c = 0; c < CP; ++c) {
         if (!C::ONE_TABLE && c >= cnt) break;
@@ -1079,11 +982,7 @@ __global__ void __launch_bounds__(512, 1)
           }
         }
       }
-#ifdef NSNKV_DEBUG_SKIP_CONSUME
-      }
-#endif
       // release the stage and the producer slot (scales, value shifts, TMEM D)
-      A3_TRACE(warp, 4, n);
       tc05::fence_before();
       mbar_arrive(&BR.empty[s]);
       mbar_arrive(&BR.free_[grp][slot]);
@@ -1108,29 +1007,12 @@ __global__ void __launch_bounds__(512, 1)
 
 using namespace nsnkv;
 
-#ifdef NSNKV_TRACE
-// copy the per-warp timelines (16 x 4096 records) to the host and clear them
-extern "C" int nsnkv_debug_trace(unsigned long long *host, int max_records, int reset) {
-  cudaDeviceSynchronize();
-  const int n = 16 * 4096 < max_records ? 16 * 4096 : max_records;
-  if (host && n) cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n);
-  if (reset) {
-    static unsigned long long zero[16 * 4096];
-    cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
-  }
-  return n;
-}
-#endif
 
 template <int G, bool FOLD, int PREC>
 int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, float *lse,
                          float *recs, int64_t total, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attend3_kernel<G, FOLD, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         ATT_SMEM_BYTES);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  set_smem_attr_once(attend3_kernel<G, FOLD, PREC>, ATT_SMEM_BYTES, attr);
   int launches = 0;
   if (total > 0) {
     attend3_kernel<G, FOLD, PREC><<<grid, 512, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);

@@ -571,18 +571,9 @@ extern "C" int nsnkv_encode_chunks(const float *residual, int32_t n_resid, const
   int rc = nsnkv_internal_codebook_dev(cb, &dev);
   if (rc) return rc;
   const size_t smem = sizeof(EncodeSmem);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(encode_chunks_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(encode_chunks_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(encode_chunks_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         100);
-    cudaFuncSetAttribute(encode_chunks_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         100);
-    attr_set = true;
-  }
+  static unsigned long long attr_k = 0, attr_v = 0;
+  set_smem_attr_once(encode_chunks_kernel<true>, (int)smem, attr_k, 100);
+  set_smem_attr_once(encode_chunks_kernel<false>, (int)smem, attr_v, 100);
   const int64_t blocks = (int64_t)n_units * n_flush;
   auto kern = dev.bit_mode == 2 ? encode_chunks_kernel<true> : encode_chunks_kernel<false>;
   kern<<<(unsigned)blocks, ENC_THREADS, smem, (cudaStream_t)stream>>>(

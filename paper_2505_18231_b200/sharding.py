@@ -88,16 +88,26 @@ def plan_shards(batch: int, n_kv_heads: int, n_q_heads: int, world: int, rank: i
     return ShardPlan(world, rank, batch, n_kv_heads, n_q_heads, b, b + 1, j * hb, (j + 1) * hb)
 
 
-def gather_outputs(plan: ShardPlan, out_local: torch.Tensor, group=None) -> torch.Tensor:
+def gather_buffer(plan: ShardPlan, out_local: torch.Tensor) -> torch.Tensor:
+    """Pre-allocated receive buffer for gather_outputs (allocate once, reuse
+    every step)."""
+    return torch.empty(plan.world * out_local.numel(), dtype=out_local.dtype,
+                       device=out_local.device)
+
+
+def gather_outputs(plan: ShardPlan, out_local: torch.Tensor, group=None,
+                   buf: torch.Tensor | None = None) -> torch.Tensor:
     """All-gather the per-rank [B_local, Hq_local, d] outputs into the full
-    [B, Hq, d] tensor (one collective; equal block sizes by construction)."""
+    [B, Hq, d] tensor (one collective; equal block sizes by construction).
+    `buf` (from gather_buffer) avoids an allocation per step."""
     import torch.distributed as dist
 
     d = out_local.shape[-1]
-    if plan.world == 1:
+    if plan.world == 1 and not dist.is_initialized():
         return out_local
-    flat = torch.empty(plan.world * out_local.numel(), dtype=out_local.dtype,
-                       device=out_local.device)
+    flat = buf if buf is not None else gather_buffer(plan, out_local)
+    if flat.numel() != plan.world * out_local.numel():
+        raise ValueError("gather buffer has the wrong size")
     dist.all_gather_into_tensor(flat, out_local.contiguous().view(-1), group=group)
     blocks = flat.view(plan.world, plan.local_batch, plan.local_q_heads, d)
     if plan.by_batch:
@@ -116,6 +126,7 @@ class ShardedDecoder:
         self.plan = plan
         self.cache = local_cache
         self.group = group
+        self._buf = None
 
     def append(self, keys: torch.Tensor, values: torch.Tensor):
         self.cache.append(self.plan.kv_slice(keys).contiguous(),
@@ -124,4 +135,6 @@ class ShardedDecoder:
 
     def attend(self, q: torch.Tensor) -> torch.Tensor:
         out_local = self.cache.attend(self.plan.q_slice(q).contiguous())
-        return gather_outputs(self.plan, out_local, self.group)
+        if self._buf is None or self._buf.numel() != self.plan.world * out_local.numel():
+            self._buf = gather_buffer(self.plan, out_local)
+        return gather_outputs(self.plan, out_local, self.group, self._buf)

@@ -102,3 +102,40 @@ def level1_inputs():
     v[5] = np.float32(3.0e30)
     match["edge"] = (v, e, True)
     return {"fwht": fwht, "match": match}
+
+
+# BASELINE configs[0] (C1): 8 KV heads x (4096 + 37) tokens, GQA 4, batch 1
+C1_HEADS, C1_TOKENS, C1_G = 8, 4096 + 37, 4
+C1_CASES = [
+    # name, bit_mode, dist, seed, distinct value codebook
+    ("2b_normal", 2, "normal", 31, False),
+    ("2b_mis", 2, "mis", 32, True),
+    ("1b_normal", 1, "normal", 33, False),
+    ("1b_mis", 1, "mis", 34, True),
+]
+
+
+def c1_value_entries(entries: np.ndarray, distinct: bool) -> np.ndarray:
+    """Value codebook of a C1 case: the key codebook itself, or a different
+    valid codebook (rows permuted by a fixed stride, scaled by 1.25) so a K/V
+    codebook swap anywhere in the GPU path changes the result."""
+    e = np.ascontiguousarray(entries, np.float32)
+    if not distinct:
+        return e
+    perm = (np.arange(256) * 37 + 11) % 256
+    return np.ascontiguousarray(e[perm] * np.float32(1.25))
+
+
+def c1_inputs():
+    for name, bm, dist, seed, distinct in C1_CASES:
+        g = rng(seed)
+        if dist == "normal":
+            K = g.standard_normal((C1_HEADS, C1_TOKENS, D), dtype=np.float32)
+            V = g.standard_normal((C1_HEADS, C1_TOKENS, D), dtype=np.float32)
+        else:
+            K = np.stack([misaligned(g, C1_TOKENS) for _ in range(C1_HEADS)])
+            V = np.stack([misaligned(g, C1_TOKENS) for _ in range(C1_HEADS)])
+        q = np.stack([_q_roped(g, C1_G, C1_TOKENS - 1) for _ in range(C1_HEADS)])
+        yield {"name": name, "bit_mode": bm, "distinct_v": distinct,
+               "batches": [(0, 3001), (3001, C1_TOKENS)],
+               "keys": K, "values_ht": V, "q": q}

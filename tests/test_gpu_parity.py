@@ -159,9 +159,9 @@ def test_fused_precision_modes_vs_reference(case):
 
     g = load_golden(f"pipeline_{case['name']}.npz")
     cb = codebook_for(case["bit_mode"])
-    # 1-bit: plain fp16 scores miss the tolerance on the misaligned fixture
-    # (1.25e-3), so only "precise" is offered as a 1-bit default
-    modes = ("precise",) + (("balanced", "fast") if cb.bit_mode == 2 else ())
+    # key codewords are always hi + lo; 2-bit may use plain fp16 value
+    # codewords ("vfast"), 1-bit may not (cache.default_precision)
+    modes = ("precise",) + (("vfast",) if cb.bit_mode == 2 else ())
     for prec in modes:
         cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode, strategy=P.ScaleStrategy(case["strategy"]))
         c = P.PagedKvCache(cfg, 1, 1, cb_k=cb, cb_v=cb, base_position=case["base_position"],

@@ -204,3 +204,41 @@ def test_bench_step_bytes_and_clock_summary():
     s = cs.summary()
     assert s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0
     assert s["reasons"] == ["sw_power_cap"] and s["samples"] == 3
+
+
+def test_precision_policy():
+    """Key codewords are always hi + lo; plain-fp16 modes that are known to
+    exceed the 1e-3 tolerance need an explicit opt-in."""
+    from paper_2505_18231_b200.cache import PRECISIONS, check_precision, default_precision
+    from paper_2505_18231_b200.errors import Unsupported
+
+    assert default_precision(2) == "vfast" and default_precision(1) == "precise"
+    assert check_precision("precise", 1) == "precise"
+    assert check_precision("vfast", 2) == "vfast"
+    for prec, bm in (("fast", 2), ("fast", 1), ("vfast", 1)):
+        with pytest.raises(Unsupported):
+            check_precision(prec, bm)
+        assert check_precision(prec, bm, allow_inexact=True) == prec
+    with pytest.raises(ValueError):
+        check_precision("balanced", 2)
+    assert PRECISIONS == {"precise": 0, "vfast": 1, "fast": 2}
+
+
+def test_wire_field_diff_counts():
+    """tests/wirediff.py classifies byte differences per field."""
+    import numpy as np
+
+    from tests.conftest import load_golden
+    from tests.wirediff import compare
+
+    g = load_golden("pipeline_2b_normal.npz")
+    ref = g["k_wire"]
+    got = ref.copy()
+    got[0, 6 + 5] ^= 1              # one index byte
+    got[1, 6 + 1024 + 3] ^= 0x81    # two sign bits
+    s2 = 6 + 2048 + 36 + 80
+    v = got[2, s2:s2 + 2].view("<u2")
+    v[0] += 1                       # one f16 ulp
+    c = compare(got, ref, 2)
+    assert c["idx_flips"] == 1 and c["signs_flips"] == 2
+    assert c["s2_diffs"] == 1 and c["s2_max_ulp"] == 1

@@ -96,3 +96,37 @@ def test_sharded_decode_matches_single_process(B, Hkv, Hq, world):
     mp.spawn(_worker, args=(world, _free_port(), B, Hkv, Hq, T, q, k, v, ret), nprocs=world,
              join=True)
     assert np.array_equal(ret["out"], want)
+
+
+@pytest.mark.gpu
+def test_nccl_gather_outputs_one_rank_with_paged_cache():
+    """The NCCL all-gather path on a real GPU (one rank, so it runs on the
+    one-GPU test box): ShardedDecoder over a PagedKvCache returns the local
+    cache's own output, through all_gather_into_tensor into the reused
+    pre-allocated buffer."""
+    import paper_2505_18231_b200 as P
+    from paper_2505_18231_b200.sharding import ShardedDecoder
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                            device_id=torch.device("cuda", 0))
+    try:
+        B, Hkv, Hq, T = 2, 4, 16, 64 * 5 + 9
+        cb = P.default_codebook("2b")
+        cache = P.PagedKvCache(P.CacheConfig(d=128, bit_mode=cb.bit_mode), B, Hkv, cb_k=cb, cb_v=cb)
+        dec = ShardedDecoder(plan_shards(B, Hkv, Hq, 1, 0), cache)
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1)
+        dec.append(torch.randn(B, Hkv, T, 128, device="cuda", generator=g),
+                   torch.randn(B, Hkv, T, 128, device="cuda", generator=g))
+        q = torch.randn(B, Hq, 128, device="cuda", generator=g)
+        full = dec.attend(q)
+        buf = dec._buf
+        assert buf is not None and full.shape == (B, Hq, 128)
+        assert torch.equal(full, cache.attend(q))
+        dec.attend(q)
+        assert dec._buf is buf  # reused, not re-allocated
+    finally:
+        dist.destroy_process_group()
