@@ -30,7 +30,7 @@ def _oracle(cache, unit, n, q_unit):
 
 
 @pytest.mark.parametrize("mode,G,precision,counts", [
-    ("2b", 4, "fast", [0, 1, 2, 3, 9, 5, 0, 7, 1, 4, 8, 6]),
+    ("2b", 4, "vfast", [0, 1, 2, 3, 9, 5, 0, 7, 1, 4, 8, 6]),
     ("2b", 4, "precise", [3, 0, 1, 9, 2, 2, 5, 0, 7, 1, 9, 4]),
     ("2b", 1, None, [1, 0, 0, 2, 3, 1, 5, 0, 1, 1, 2, 1]),   # 17 chunks: grid of 17 CTAs
     ("1b", 8, None, [9, 9, 9, 9, 9, 9, 9, 9, 9, 9, 9, 0]),
