@@ -459,7 +459,7 @@ class PagedKvCache:
 
     def wire_chunks(self, unit: int, kind: str = "k") -> np.ndarray:
         """[n_chunks, wire_bytes] reference serialized chunks of one unit."""
-        return pages_to_wire(self.pages(unit, kind), self.bit_mode, self.config.strategy)
+        return pages_to_wire(self.pages(unit, kind), self.bit_mode, self.config.strategy, kind)
 
     def chunk_wire(self, unit: int, kind: str = "k") -> list[bytes]:
         return [w.tobytes() for w in self.wire_chunks(unit, kind)]
@@ -513,14 +513,39 @@ def permute_signs(signs: np.ndarray) -> np.ndarray:
     return words
 
 
+def unpermute_signs_v(words: np.ndarray) -> np.ndarray:
+    """[..., 256] u32 value-page sign words -> natural sign bytes [..., 64, 16].
+    Word 8 i + c holds component c of token pair (2i, 2i+1): bit j = token
+    2i, sub j; bit 16 + j = token 2i+1 (see csrc/encode.cu)."""
+    w = words.astype(np.uint32).reshape(words.shape[:-1] + (32, 8))
+    out = np.zeros(words.shape[:-1] + (32, 2, 16), np.uint32)
+    for c in range(8):
+        for j in range(16):
+            out[..., 0, j] |= ((w[..., c] >> j) & 1) << c
+            out[..., 1, j] |= ((w[..., c] >> (16 + j)) & 1) << c
+    return out.reshape(words.shape[:-1] + (64, 16)).astype(np.uint8)
+
+
+def permute_signs_v(signs: np.ndarray) -> np.ndarray:
+    """Natural sign bytes [..., 64, 16] -> value-page words [..., 256] u32."""
+    s = signs.astype(np.uint32).reshape(signs.shape[:-2] + (32, 2, 16))
+    w = np.zeros(signs.shape[:-2] + (32, 8), np.uint32)
+    for c in range(8):
+        for j in range(16):
+            w[..., c] |= ((s[..., 0, j] >> c) & 1) << j
+            w[..., c] |= ((s[..., 1, j] >> c) & 1) << (16 + j)
+    return w.reshape(signs.shape[:-2] + (256,))
+
+
 def wire_bytes(bit_mode) -> int:
     """Bytes of one serialized chunk (vq.py:363-380)."""
     return 6 + 1024 + (1024 if int(bit_mode) == 2 else 0) + 36 + 80 + 128
 
 
-def pages_to_wire(pages: np.ndarray, bit_mode, strategy) -> np.ndarray:
+def pages_to_wire(pages: np.ndarray, bit_mode, strategy, kind: str = "k") -> np.ndarray:
     """[n, page_bytes] device pages -> [n, wire_bytes] reference serialized
-    chunks (vq.py:363-380), vectorised over chunks."""
+    chunks (vq.py:363-380), vectorised over chunks.  kind "k" / "v": key and
+    value pages order their sign bits for their own decode side."""
     bm = BitMode(bit_mode)
     o_idx, o_sgn, o_s2, o_s1n, o_on, o_par = _LAYOUT[bm]
     p = np.ascontiguousarray(pages, dtype=np.uint8).reshape(-1, PAGE_BYTES[bm])
@@ -531,8 +556,9 @@ def pages_to_wire(pages: np.ndarray, bit_mode, strategy) -> np.ndarray:
     out[:, pos:pos + 1024] = p[:, o_idx:o_idx + 1024]
     pos += 1024
     if bm is BitMode.TWO_BIT:
-        w = p[:, o_sgn:o_sgn + 1024].copy().view("<u4").reshape(n, R, 4)
-        out[:, pos:pos + 1024] = unpermute_signs(w).reshape(n, 1024)
+        w = p[:, o_sgn:o_sgn + 1024].copy().view("<u4")
+        nat = unpermute_signs(w.reshape(n, R, 4)) if kind == "k" else unpermute_signs_v(w)
+        out[:, pos:pos + 1024] = nat.reshape(n, 1024)
         pos += 1024
     par = p[:, o_par:o_par + 20]
     out[:, pos:pos + 4] = par[:, 0:4]                       # s1 scale, zero
@@ -549,11 +575,12 @@ def pages_to_wire(pages: np.ndarray, bit_mode, strategy) -> np.ndarray:
     return out
 
 
-def page_to_wire(page: np.ndarray, bit_mode: BitMode, strategy: ScaleStrategy) -> bytes:
-    return pages_to_wire(np.asarray(page)[None], bit_mode, strategy)[0].tobytes()
+def page_to_wire(page: np.ndarray, bit_mode: BitMode, strategy: ScaleStrategy,
+                 kind: str = "k") -> bytes:
+    return pages_to_wire(np.asarray(page)[None], bit_mode, strategy, kind)[0].tobytes()
 
 
-def wire_to_page(blob: bytes) -> np.ndarray:
+def wire_to_page(blob: bytes, kind: str = "k") -> np.ndarray:
     """Inverse of page_to_wire (for loading reference-serialized chunks)."""
     n, d, bm_raw, _strategy = struct.unpack_from("<HHBB", blob, 0)
     if n != R or d != D:
@@ -566,7 +593,9 @@ def wire_to_page(blob: bytes) -> np.ndarray:
     page[o_idx:o_idx + 1024] = b[pos:pos + 1024]
     pos += 1024
     if bm is BitMode.TWO_BIT:
-        page[o_sgn:o_sgn + 1024] = permute_signs(b[pos:pos + 1024].reshape(R, 16)).view(np.uint8).ravel()
+        nat = b[pos:pos + 1024].reshape(R, 16)
+        words = permute_signs(nat) if kind == "k" else permute_signs_v(nat)
+        page[o_sgn:o_sgn + 1024] = words.astype("<u4").view(np.uint8).ravel()
         pos += 1024
     par = np.zeros(10, "<u2")
     par[0], par[1] = struct.unpack_from("<HH", blob, pos)

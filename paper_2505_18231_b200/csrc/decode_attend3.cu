@@ -476,7 +476,16 @@ __global__ void __launch_bounds__(512, 1)
           }
           SL.sc[c][2 * lane] = v0;
           SL.sc[c][2 * lane + 1] = v1;
-          *reinterpret_cast<float4 *>(&SL.ov[c][4 * lane]) = o4;
+          // value shift channel ch = 16 mt + 8 h + g stored at 16 g + 2 mt + h:
+          // a consumer lane reads its 16 accumulator rows as four float4
+          {
+            const float ov4[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int ch = 4 * lane + e;
+              SL.ov[c][16 * (ch & 7) + 2 * (ch >> 4) + ((ch >> 3) & 1)] = ov4[e];
+            }
+          }
         }
         }
         // the MMA chain that last used this Z buffer (batch m - NZB) is done
@@ -593,8 +602,12 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t lbk = (tab_k & 0xffff0000u) | (tab_k & 0xffu) | slot16;
     const uint32_t lbv = (tab_v & 0xffff0000u) | (tab_v & 0xffu) | slot16;
     constexpr uint32_t LO_OFS = C::ONE_TABLE ? 0u : 128u;  // hi -> lo half of an entry
-    const uint32_t vsel0 = 0x7604u | ((uint32_t)(2 * (g & 1)) << 4);
-    const uint32_t vsel1 = 0x7604u | ((uint32_t)(2 * (g & 1) + 1) << 4);
+    // V side (ldmatrix.x4.trans): lane supplies the row address of token
+    // vT (of the warp's 16) for sub 2 mt + vodd; the index byte sits in word
+    // mt / 2 at byte 2 (mt & 1) + vodd
+    const int vT = (lane & 7) + 8 * (lane >> 4), vodd = (lane >> 3) & 1;
+    const uint32_t vselA = 0x7604u | ((uint32_t)vodd << 4);
+    const uint32_t vselB = 0x7604u | ((uint32_t)(2 + vodd) << 4);
     const uint32_t psel = (g & 1) ? 0x7632u : 0x5410u;
 
     uint32_t qB[NTP][8][2];
@@ -642,15 +655,15 @@ __global__ void __launch_bounds__(512, 1)
             if (r > 0) {
 #pragma unroll
               for (int mt = 0; mt < 8; ++mt) {
-                const int c = 16 * g + 8 * (mt >> 2) + 2 * (mt & 3);
+                const int c = 16 * mt + g;  // accumulator rows g / g + 8 of m-tile mt
                 float a0 = (accV[nt][mt][0] + accV[nt][mt][1]) * sa;
                 float a1 = (accV[nt][mt][2] + accV[nt][mt][3]) * sa;
                 if (r < 3) {
                   a0 = fmaf(S.mg.acc[h][c], sb, a0);
-                  a1 = fmaf(S.mg.acc[h][c + 1], sb, a1);
+                  a1 = fmaf(S.mg.acc[h][c + 8], sb, a1);
                 }
                 S.mg.acc[h][c] = a0;
-                S.mg.acc[h][c + 1] = a1;
+                S.mg.acc[h][c + 8] = a1;
               }
               mnew[nt] = m;
               lnew[nt] = l;
@@ -658,10 +671,9 @@ __global__ void __launch_bounds__(512, 1)
               float *rec = record_ptr<G>(recs, (unit + blockIdx.x) * NGRP + grp) + h * (4 + D);
 #pragma unroll
               for (int mt = 0; mt < 8; ++mt) {
-                const int c = 16 * g + 8 * (mt >> 2) + 2 * (mt & 3);
-                const float a0 = fmaf(S.mg.acc[h][c], sb, (accV[nt][mt][0] + accV[nt][mt][1]) * sa);
-                const float a1 = fmaf(S.mg.acc[h][c + 1], sb, (accV[nt][mt][2] + accV[nt][mt][3]) * sa);
-                *reinterpret_cast<float2 *>(rec + 4 + c) = make_float2(a0, a1);
+                const int c = 16 * mt + g;
+                rec[4 + c] = fmaf(S.mg.acc[h][c], sb, (accV[nt][mt][0] + accV[nt][mt][1]) * sa);
+                rec[4 + c + 8] = fmaf(S.mg.acc[h][c + 8], sb, (accV[nt][mt][2] + accV[nt][mt][3]) * sa);
               }
               if (g == 0) {
                 rec[0] = m;
@@ -919,66 +931,56 @@ __global__ void __launch_bounds__(512, 1)
       }
 
       // ---- V side: accumulate P' . codewords on tensor cores -----------------
-      const int vt0 = 16 * ws + 2 * t;
+      // A = codewords^T [channel][token] straight from the gather table with
+      // ldmatrix.trans (each lane one 16-byte codeword row; replica slot =
+      // row in the 8x8 matrix, so every phase is conflict-free); m-tile mt =
+      // channels 16 mt .. 16 mt + 15 (subs 2 mt, 2 mt + 1), k = the warp's
+      // 16 tokens.  Value-page sign words are stored in this fragment order
+      // (encode.cu): word 8 i + c = component c of token pair (2i, 2i+1).
 #pragma unroll
       for (int c = 0; c < CP; ++c) {
         if (!C::ONE_TABLE && c >= cnt) break;
         const uint32_t vpa = smem_u32(st + c * 2 * C::MAIN + C::MAIN);
-        uint32_t iv[4], sv[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tok = vt0 + (q & 1) + ((q & 2) ? 8 : 0);
-          iv[q] = lds32(vpa + L.idx + tok * NSUB + 4 * (g >> 1));
-          sv[q] = FOLD ? (lds32(vpa + (FOLD ? L.sgn : 0) + tok * 16 + 4 * (g >> 1)) >> (8 * (g & 1))) : 0u;
+        const uint4 iw = lds128(vpa + L.idx + (16 * ws + vT) * NSUB);
+        uint32_t sw0 = 0, sw1 = 0;
+        if (FOLD) {
+          sw0 = lds32(vpa + (FOLD ? L.sgn : 0) + ((8 * ws + t) * 8 + g) * 4);
+          sw1 = lds32(vpa + (FOLD ? L.sgn : 0) + ((8 * ws + 4 + t) * 8 + g) * 4);
         }
+        const uint32_t iwv[4] = {iw.x, iw.y, iw.z, iw.w};
 #pragma unroll
-        for (int sg = 0; sg < 2; ++sg) {
-          const uint32_t sel = sg ? vsel1 : vsel0;
-          uint4 yh[4], yl[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t a = prmt(iv[q], lbv, sel);
-            yh[q] = lds128(a);
-            yl[q] = HILO_V ? lds128(a + LO_OFS) : make_uint4(0, 0, 0, 0);
-            if (FOLD) {
-              uint32_t *ph = &yh[q].x, *pl = &yl[q].x;
-#pragma unroll
-              for (int p = 0; p < 4; ++p) {
-                const uint32_t wk = sv[q] << (15 - 4 * sg - p);
-                ph[p] = xor_sign(ph[p], wk);
-                if (HILO_V) pl[p] = xor_sign(pl[p], wk);
-              }
-            }
-          }
-#pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            const int mt = 4 * sg + p;
-            const uint32_t *h0p = &yh[0].x, *h1p = &yh[1].x, *h2p = &yh[2].x, *h3p = &yh[3].x;
-            const uint32_t a0h = prmt(h0p[p], h1p[p], 0x5410u), a1h = prmt(h0p[p], h1p[p], 0x7632u);
-            const uint32_t a2h = prmt(h2p[p], h3p[p], 0x5410u), a3h = prmt(h2p[p], h3p[p], 0x7632u);
-#pragma unroll
-            for (int nt = 0; nt < NTP; ++nt)
-              mma16816(accV[nt][mt], a0h, a1h, a2h, a3h, pf[c][nt][0], pf[c][nt][1]);
+        for (int mt = 0; mt < 8; ++mt) {
+          const uint32_t a = prmt(iwv[mt >> 1], lbv, (mt & 1) ? vselB : vselA);
+          uint32_t x[4], y[4] = {0u, 0u, 0u, 0u};
+          ldsm_x4_trans(a, x);
+          if (HILO_V) ldsm_x4_trans(a + LO_OFS, y);
+          if (FOLD) {
+            const uint32_t m0 = sw0 << (15 - 2 * mt), m1 = sw0 << (14 - 2 * mt);
+            const uint32_t m2 = sw1 << (15 - 2 * mt), m3 = sw1 << (14 - 2 * mt);
+            x[0] = xor_sign(x[0], m0); x[1] = xor_sign(x[1], m1);
+            x[2] = xor_sign(x[2], m2); x[3] = xor_sign(x[3], m3);
             if (HILO_V) {
-              const uint32_t *l0p = &yl[0].x, *l1p = &yl[1].x, *l2p = &yl[2].x, *l3p = &yl[3].x;
-              const uint32_t a0l = prmt(l0p[p], l1p[p], 0x5410u), a1l = prmt(l0p[p], l1p[p], 0x7632u);
-              const uint32_t a2l = prmt(l2p[p], l3p[p], 0x5410u), a3l = prmt(l2p[p], l3p[p], 0x7632u);
-#pragma unroll
-              for (int nt = 0; nt < NTP; ++nt)
-                mma16816(accV[nt][mt], a0l, a1l, a2l, a3l, pf[c][nt][0], pf[c][nt][1]);
+              y[0] = xor_sign(y[0], m0); y[1] = xor_sign(y[1], m1);
+              y[2] = xor_sign(y[2], m2); y[3] = xor_sign(y[3], m3);
             }
           }
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const float4 o4 = *reinterpret_cast<const float4 *>(&SL.ov[c][16 * g + 4 * q4]);
-          const int mt0 = 4 * (q4 >> 1) + 2 * (q4 & 1);
 #pragma unroll
           for (int nt = 0; nt < NTP; ++nt) {
-            accV[nt][mt0][0] = fmaf(wsum[c][nt], o4.x, accV[nt][mt0][0]);
-            accV[nt][mt0][2] = fmaf(wsum[c][nt], o4.y, accV[nt][mt0][2]);
-            accV[nt][mt0 + 1][0] = fmaf(wsum[c][nt], o4.z, accV[nt][mt0 + 1][0]);
-            accV[nt][mt0 + 1][2] = fmaf(wsum[c][nt], o4.w, accV[nt][mt0 + 1][2]);
+            mma16816(accV[nt][mt], x[0], x[1], x[2], x[3], pf[c][nt][0], pf[c][nt][1]);
+            if (HILO_V) mma16816(accV[nt][mt], y[0], y[1], y[2], y[3], pf[c][nt][0], pf[c][nt][1]);
+          }
+        }
+        // value shift o' of the chunk: rows 16 mt + g, 16 mt + 8 + g
+        const float *ovp = &SL.ov[c][16 * g];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 o4 = *reinterpret_cast<const float4 *>(ovp + 4 * q4);
+#pragma unroll
+          for (int nt = 0; nt < NTP; ++nt) {
+            accV[nt][2 * q4][0] = fmaf(wsum[c][nt], o4.x, accV[nt][2 * q4][0]);
+            accV[nt][2 * q4][2] = fmaf(wsum[c][nt], o4.y, accV[nt][2 * q4][2]);
+            accV[nt][2 * q4 + 1][0] = fmaf(wsum[c][nt], o4.z, accV[nt][2 * q4 + 1][0]);
+            accV[nt][2 * q4 + 1][2] = fmaf(wsum[c][nt], o4.w, accV[nt][2 * q4 + 1][2]);
           }
         }
       }

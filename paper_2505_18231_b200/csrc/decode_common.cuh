@@ -55,7 +55,9 @@ __device__ __forceinline__ float dequant_o(const uint8_t *page, const PageLayout
   return __fadd_rn(m.o_zero[g], __fmul_rn((float)nibble(page + L.on, c), m.o_scale[g]));
 }
 
-// Natural sign byte of (token t, sub j) from the bit-permuted page words.
+// Natural sign byte of (token t, sub j) of a KEY page (decode K order: word
+// q of token t covers subs 4q+m; bit 4m+p = sign of component 2p, bit
+// 16+4m+p = sign of component 2p+1).
 __device__ __forceinline__ uint32_t sign_byte(const uint8_t *page, const PageLayout &L, int t,
                                               int j) {
   const uint32_t w = reinterpret_cast<const uint32_t *>(page + L.sgn)[4 * t + (j >> 2)];
@@ -66,6 +68,19 @@ __device__ __forceinline__ uint32_t sign_byte(const uint8_t *page, const PageLay
     b |= ((w >> (4 * m + p)) & 1u) << (2 * p);
     b |= ((w >> (16 + 4 * m + p)) & 1u) << (2 * p + 1);
   }
+  return b;
+}
+
+// Natural sign byte of (token t, sub j) of a VALUE page (decode V order: word
+// 8 i + c holds component c of token pair (2i, 2i+1); bit j = token 2i, sub
+// j; bit 16 + j = token 2i+1).
+__device__ __forceinline__ uint32_t sign_byte_v(const uint8_t *page, const PageLayout &L, int t,
+                                                int j) {
+  const uint32_t *w = reinterpret_cast<const uint32_t *>(page + L.sgn) + 8 * (t >> 1);
+  const int sh = j + 16 * (t & 1);
+  uint32_t b = 0;
+#pragma unroll
+  for (int c = 0; c < SUB; ++c) b |= ((w[c] >> sh) & 1u) << c;
   return b;
 }
 

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(128) output_partial_kernel(CacheViewDev cv,
     for (int t = 0; t < R; ++t) {
       const int e = page[L.idx + t * NSUB + j];
       float cval = s_ent[e * 8 + k];
-      if (L.sgn >= 0 && ((sign_byte(page, L, t, j) >> k) & 1u)) cval = -cval;
+      if (L.sgn >= 0 && ((sign_byte_v(page, L, t, j) >> k) & 1u)) cval = -cval;
       const float s1 = dequant_s1(page, L, m, t);
       const float s2 = f16_bits_to_f32(reinterpret_cast<const uint16_t *>(page + L.s2)[t]);
       const float row = s1 * (s2 * cval + o);  // attention.py:126-128

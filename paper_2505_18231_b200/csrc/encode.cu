@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
     const uint32_t w = *reinterpret_cast<const uint32_t *>(&s.idx[0][0] + 4 * tid);
     *reinterpret_cast<uint32_t *>(page + L.idx + 4 * tid) = w;
   }
-  if (fold) {  // bit-permuted signs: word q of token t covers subs 4q..4q+3
+  if (fold && is_key) {  // key signs, decode K order: word q of token t covers subs 4q..4q+3
     const int t = tid >> 2, q = tid & 3;
     uint32_t w = 0;
 #pragma unroll
@@ -483,6 +483,16 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
         w |= ((b >> (2 * p)) & 1u) << (4 * m + p);
         w |= ((b >> (2 * p + 1)) & 1u) << (16 + 4 * m + p);
       }
+    }
+    *reinterpret_cast<uint32_t *>(page + L.sgn + 4 * tid) = w;
+  } else if (fold) {  // value signs, decode V order: word 8 i + c = component c of
+    // token pair (2i, 2i+1); bit j = token 2i, sub j; bit 16 + j = token 2i+1
+    const int i = tid >> 3, c = tid & 7;
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < NSUB; ++j) {
+      w |= ((uint32_t)(s.sgn[2 * i][j] >> c) & 1u) << j;
+      w |= ((uint32_t)(s.sgn[2 * i + 1][j] >> c) & 1u) << (16 + j);
     }
     *reinterpret_cast<uint32_t *>(page + L.sgn + 4 * tid) = w;
   }

@@ -43,7 +43,7 @@ def _wire_all(cache, kind):
     ids = cache.page_table[:, :cache.n_chunks].reshape(-1).long()
     from paper_2505_18231_b200.cache import pages_to_wire
 
-    return pages_to_wire(pool[ids].cpu().numpy(), cache.bit_mode, cache.config.strategy)
+    return pages_to_wire(pool[ids].cpu().numpy(), cache.bit_mode, cache.config.strategy, kind)
 
 
 @pytest.mark.parametrize("mode,dist", [("2b", "normal"), ("1b", "mis")])

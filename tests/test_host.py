@@ -84,10 +84,25 @@ def test_page_wire_roundtrip_on_reference_chunks(name):
         for blob in g[f"{kind}_wire"]:
             blob = blob.tobytes()
             bm = blob[4]
-            page = wire_to_page(blob)
+            page = wire_to_page(blob, kind)
             assert page.size == PAGE_BYTES[bm]
             assert not page[LEDGER_BYTES[bm]:].any()  # padding stays zero
-            assert page_to_wire(page, bm, blob[5]) == blob
+            assert page_to_wire(page, bm, blob[5], kind) == blob
+
+
+def test_value_sign_layout_is_a_bijection():
+    """Value pages order their sign bits for the ldmatrix.trans fragments:
+    word 8 i + c = component c of token pair (2i, 2i+1)."""
+    from paper_2505_18231_b200.cache import permute_signs_v, unpermute_signs_v
+
+    rng = np.random.default_rng(2)
+    s = rng.integers(0, 256, (3, 64, 16)).astype(np.uint8)
+    w = permute_signs_v(s)
+    assert w.shape == (3, 256)
+    assert np.array_equal(unpermute_signs_v(w), s)
+    # token 2i+1, sub j, component c lives at bit 16 + j of word 8 i + c
+    t, j, c = 37, 5, 6
+    assert ((w[1, 8 * (t // 2) + c] >> (16 + j)) & 1) == ((s[1, t, j] >> c) & 1)
 
 
 def test_sign_permutation_is_a_bijection():
