@@ -1,8 +1,7 @@
 // decode_dispatch.cu -- nsnkv_decode_attend entry point: validates the cache
 // view, sizes the stream-K record workspace and dispatches to the fused
-// kernel instantiation for (GQA group, bit mode, precision).  The kernels
-// themselves live in decode_attend3.cu (2-bit, and 1-bit `precise`) and
-// decode_lut1.cu (1-bit: K-side query-codeword lookup tables).
+// kernel instantiation for (GQA group, bit mode, precision).  The kernel
+// itself lives in decode_attend3.cu.
 #include <cstdlib>
 #include <cstring>
 
