@@ -478,10 +478,11 @@ def c1_parity() -> dict:
 
 
 def measure_serving(cache, q, steps: int) -> dict:
-    """One decode step as a server runs it: append this step's K/V token for
-    every (sequence, kv-head) -- a 64-token chunk is flushed through the
-    encode kernel every 64 steps -- then attend.  Averaged over `steps`
-    steps (a multiple of 64, so the flushes are included)."""
+    """One decode step as a server runs it (PagedKvCache.decode_step): append
+    this step's K/V token for every (sequence, kv-head) and attend over the
+    cache including it -- in the attend launches when no chunk completes, a
+    64-token chunk flushed through nsnkv_append every 64 steps.  Averaged
+    over `steps` steps (a multiple of 64, so the flushes are included)."""
     import torch
 
     B, Hkv = cache.batch, cache.n_kv_heads
@@ -496,12 +497,12 @@ def measure_serving(cache, q, steps: int) -> dict:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(steps):
-        cache.append(ks[i], vs[i])
-        cache.attend(q, out=out)
+        cache.decode_step(q, ks[i], vs[i], out=out)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    return {"what": "append 1 token/sequence (flush every 64) + attend", "ms_per_step": round(ms, 4),
+    return {"what": "PagedKvCache.decode_step: append 1 token/sequence (flush every 64) + attend",
+            "ms_per_step": round(ms, 4),
             "tokens_per_s": round(B / (ms * 1e-3), 1), "steps": steps,
             "context_after": cache.total_tokens}
 

@@ -25,6 +25,14 @@
  *   nsnkv_decode_output    -> attention.py:114-133 (output_quantized), batched
  *   nsnkv_decode_attend    -> attention.py:136-142 (attend_quantized), fused
  *                             flash-decoding, batched over (batch, q-head)
+ *   nsnkv_decode_step      -> kvcache.py:157-195 + attention.py:136-142: a
+ *                             serving decode step (append without a flush,
+ *                             then attend) in the attend launches
+ *   nsnkv_append           -> kvcache.py:157-195 (append): residual policy,
+ *                             flushes and bookkeeping of a batch of units
+ *   nsnkv_pool_*, nsnkv_pages_copy -> (no reference counterpart: the
+ *                             reference keeps chunks in Python lists) page
+ *                             storage and kvcache.py:198-213 snapshot I/O
  */
 #ifndef NSNKV_B200_H
 #define NSNKV_B200_H
@@ -145,6 +153,69 @@ int nsnkv_encode_chunks(const float *residual, int32_t n_resid,
                         int32_t page_id_stride, int32_t *counters,
                         void *stream);
 
+/* ---- serving cache: one launch per append (kvcache.py:157-195) -------- */
+/*
+ * Appends new K/V rows to every unit of a paged cache in ONE launch: all full
+ * chunks are flushed (NSN -> RoPE -> FWHT -> VQ -> pack, as
+ * nsnkv_encode_chunks) into the pages the caller allocated for them, the new
+ * residual rows are written, and the page table and per-unit counters are
+ * updated on the device (no host synchronisation).  Unit u gains
+ * new_count[u] rows (or n_new_uniform), fresh row r of unit u being row
+ * fresh_off[u] + r * fresh_row_stride of fresh_k / fresh_v ([rows][128], fp32
+ * or bf16; fresh_off NULL = u * n_new_uniform).  Unit u flushes
+ * n_flush = (n_res_in[u] + new) / 64 chunks into new_pages[u * max_flush + k]
+ * (max_flush >= every unit's n_flush), written to page_table[u][n_chunks + k].
+ * Counters are double-buffered: read from *_in, written to *_out.
+ * counters (may be NULL): [pages][2 (K, V)][NSNKV_NUM_COUNTERS] by page id.
+ */
+typedef struct nsnkv_append_args {
+  int32_t n_units;
+  int32_t max_flush;
+  const void *fresh_k;
+  const void *fresh_v;
+  int32_t fresh_bf16;
+  int64_t n_new_uniform;
+  const int32_t *new_count;  /* device [n_units] or NULL */
+  const int64_t *fresh_off;  /* device [n_units] or NULL */
+  int64_t fresh_row_stride;  /* in rows (1: [units][n][128]) */
+  float *k_res;              /* [n_units][64][128] fp32 */
+  float *v_res;
+  const int32_t *n_chunks_in;
+  const int32_t *n_res_in;
+  int32_t *n_chunks_out;
+  int32_t *n_res_out;
+  const int64_t *base_pos;   /* absolute position of each unit's token 0 */
+  int32_t *page_table;
+  int32_t page_table_stride;
+  const int32_t *new_pages;  /* device [n_units][max_flush] */
+  uint8_t *k_pool;
+  uint8_t *v_pool;
+  int32_t *counters;
+  const float *rope_cs;
+  int64_t rope_pos0;
+  int64_t rope_n;
+  const nsnkv_codebook *cb_k;
+  const nsnkv_codebook *cb_v;
+  int32_t strategy;
+} nsnkv_append_args;
+
+int nsnkv_append(const nsnkv_append_args *args, void *stream);
+
+/* Growable page pools on CUDA virtual memory: one reserved address range,
+ * physical memory mapped on demand, so growth never copies or moves a page.
+ * Created on the calling thread's current device. */
+typedef struct nsnkv_pool nsnkv_pool;
+int nsnkv_pool_create(size_t reserve_bytes, nsnkv_pool **out);
+int nsnkv_pool_reserve(nsnkv_pool *pool, size_t bytes); /* map [0, bytes) */
+void *nsnkv_pool_ptr(const nsnkv_pool *pool);
+size_t nsnkv_pool_mapped(const nsnkv_pool *pool);
+int nsnkv_pool_destroy(nsnkv_pool *pool);
+/* Copy pages ids_host[0..n) of a pool to (to_pool == 0) or from (to_pool != 0)
+ * a dense buffer of n pages in host or device memory (snapshot export /
+ * import of reference-serialized chunks). */
+int nsnkv_pages_copy(uint8_t *pool, int32_t page_bytes, const int32_t *ids_host, int32_t n,
+                     uint8_t *buf, int32_t to_pool, void *stream);
+
 /* ---- decode over the packed cache (attention.py:83-142) --------------- */
 /*
  * Cache geometry shared by the three decode entry points.  Unit u
@@ -201,6 +272,19 @@ int nsnkv_decode_output(const nsnkv_cache_view *cv, const float *weights,
 int nsnkv_decode_attend(const nsnkv_cache_view *cv, const float *q, float *out,
                         float *lse, void *workspace, size_t workspace_bytes,
                         void *stream);
+
+/* Fused serving decode step = kvcache.append of n_new (1..63) rows to every
+ * unit followed by nsnkv_decode_attend over the cache including them, with no
+ * extra launch: the combine kernel attends the new rows as residual rows and
+ * writes them into k_res / v_res.  The caller guarantees that no unit
+ * flushes (n_res[u] + n_new < 64 for every unit; otherwise use nsnkv_append
+ * first).  new_k / new_v: [units][n_new][128], fp32 or bf16 (new_bf16).
+ * n_res_out (device int32 [units], may be cv->n_res itself) receives
+ * n_res[u] + n_new. */
+int nsnkv_decode_step(const nsnkv_cache_view *cv, const float *q, const void *new_k,
+                      const void *new_v, int32_t new_bf16, int32_t n_new, int32_t *n_res_out,
+                      float *out, float *lse, void *workspace, size_t workspace_bytes,
+                      void *stream);
 
 /* Workspace bytes nsnkv_decode_attend / nsnkv_decode_output need. */
 size_t nsnkv_decode_workspace_bytes(const nsnkv_cache_view *cv);

@@ -66,6 +66,41 @@ class CacheView(ctypes.Structure):
     ]
 
 
+class AppendArgs(ctypes.Structure):
+    """Mirror of struct nsnkv_append_args."""
+
+    _fields_ = [
+        ("n_units", c_int),
+        ("max_flush", c_int),
+        ("fresh_k", c_void_p),
+        ("fresh_v", c_void_p),
+        ("fresh_bf16", c_int),
+        ("n_new_uniform", c_i64),
+        ("new_count", c_void_p),
+        ("fresh_off", c_void_p),
+        ("fresh_row_stride", c_i64),
+        ("k_res", c_void_p),
+        ("v_res", c_void_p),
+        ("n_chunks_in", c_void_p),
+        ("n_res_in", c_void_p),
+        ("n_chunks_out", c_void_p),
+        ("n_res_out", c_void_p),
+        ("base_pos", c_void_p),
+        ("page_table", c_void_p),
+        ("page_table_stride", c_int),
+        ("new_pages", c_void_p),
+        ("k_pool", c_void_p),
+        ("v_pool", c_void_p),
+        ("counters", c_void_p),
+        ("rope_cs", c_void_p),
+        ("rope_pos0", c_i64),
+        ("rope_n", c_i64),
+        ("cb_k", c_void_p),
+        ("cb_v", c_void_p),
+        ("strategy", c_int),
+    ]
+
+
 _SIGS = {
     "nsnkv_version": ([], c_int),
     "nsnkv_last_error": ([], ctypes.c_char_p),
@@ -86,9 +121,23 @@ _SIGS = {
     "nsnkv_decode_attend": ([ctypes.POINTER(CacheView), c_void_p, c_void_p, c_void_p, c_void_p,
                              c_size, c_void_p], c_int),
     "nsnkv_decode_workspace_bytes": ([ctypes.POINTER(CacheView)], c_size),
+    "nsnkv_append": ([ctypes.POINTER(AppendArgs), c_void_p], c_int),
+    "nsnkv_decode_step": ([ctypes.POINTER(CacheView), c_void_p, c_void_p, c_void_p, c_int, c_int,
+                           c_void_p, c_void_p, c_void_p, c_void_p, c_size, c_void_p], c_int),
+    "nsnkv_pool_create": ([c_size, ctypes.POINTER(c_void_p)], c_int),
+    "nsnkv_pool_reserve": ([c_void_p, c_size], c_int),
+    "nsnkv_pool_ptr": ([c_void_p], c_void_p),
+    "nsnkv_pool_mapped": ([c_void_p], c_size),
+    "nsnkv_pool_destroy": ([c_void_p], c_int),
+    "nsnkv_pages_copy": ([c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p], c_int),
 }
 
 EXPORTED = tuple(_SIGS)
+
+_missing = [n for n in _SIGS if not hasattr(lib, n)]
+if _missing:
+    raise ImportError(f"{LIB_PATH} is stale (missing {', '.join(_missing)}); rebuild it with "
+                      f"python {_PKG / 'build.py'}")
 
 for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(lib, _name)

@@ -2,7 +2,8 @@
 
 The library is the product: a C ABI (include/nsnkv_b200.h) over hand-written
 CUDA kernels.  It is built in place so the .so travels with the repository
-snapshot to the GPU box.  Usage: ``python -m paper_2505_18231_b200.build``.
+snapshot to the GPU box.  Usage: ``python paper_2505_18231_b200/build.py``
+(not ``-m``: importing the package loads the library it is about to rebuild).
 """
 
 from __future__ import annotations
@@ -17,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libnsnkv_b200.so"
 
-SOURCES = ["capi.cu", "level1.cu", "encode.cu", "decode_ref.cu", "decode_dispatch.cu", "decode_attend3.cu"]
+SOURCES = ["capi.cu", "pool.cu", "level1.cu", "encode.cu", "decode_ref.cu", "decode_dispatch.cu", "decode_attend3.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

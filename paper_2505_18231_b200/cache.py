@@ -11,18 +11,19 @@ Reference (pkg/src/nsnkv):
   * snapshot / wire format     kvcache.py:198-213, vq.py:363-380
 
 ``PagedKvCache`` holds B x H_kv independent units (one reference
-``KvCacheState`` each) in device memory: packed pages for every flushed
-64-token chunk (K and V pools), a page table, and the fp32 residual rows.
-Every unit of a batch advances by the same token count per ``append`` (the
-serving case: one decode token or one prefill block per sequence); the
-single-head facade in ``api.py`` is a 1 x 1 batch.
+``KvCacheState`` each, with its own length) in device memory: packed pages
+for every flushed 64-token chunk (K and V pools on growable virtual memory),
+a free list, a page table, and the fp32 residual rows.  Appends are uniform
+([B, H, n, 128]) or ragged (packed rows + per-sequence lengths), one kernel
+launch each; sequences are released and imported from reference snapshots.
+The single-head facade in ``api.py`` is a 1 x 1 batch.
 """
 
 from __future__ import annotations
 
-import os
-
+import ctypes
 import enum
+import os
 import math
 import struct
 from dataclasses import dataclass
@@ -32,7 +33,7 @@ import torch
 
 from . import _lib
 from .codebook import BitMode, Codebook
-from .errors import ShapeMismatch, Unsupported
+from .errors import FormatError, IndexOutOfRange, ShapeMismatch, Unsupported
 
 D = 128
 R = 64
@@ -176,8 +177,52 @@ def _stream() -> int:
 # ---------------------------------------------------------------------------
 # the batched cache
 # ---------------------------------------------------------------------------
+class _Pool:
+    """One growable page pool (C-ABI nsnkv_pool_*): a reserved virtual address
+    range with physical memory mapped on demand, so growth never copies or
+    moves a page."""
+
+    def __init__(self, device: torch.device, page_bytes: int):
+        self.page_bytes = page_bytes
+        reserve = torch.cuda.get_device_properties(device).total_memory
+        h = _lib.c_void_p()
+        with torch.cuda.device(device):
+            _lib.check(_lib.lib.nsnkv_pool_create(reserve, ctypes.byref(h)))
+        self.handle = h.value
+        self.ptr = int(_lib.lib.nsnkv_pool_ptr(self.handle))
+
+    @property
+    def pages(self) -> int:
+        return int(_lib.lib.nsnkv_pool_mapped(self.handle)) // self.page_bytes
+
+    def grow(self, pages: int) -> int:
+        """Map memory for at least `pages` pages; returns the page capacity."""
+        if pages > self.pages:
+            _lib.check(_lib.lib.nsnkv_pool_reserve(self.handle, pages * self.page_bytes))
+        return self.pages
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order varies
+        try:
+            _lib.lib.nsnkv_pool_destroy(self.handle)
+        except Exception:
+            pass
+
+
 class PagedKvCache:
-    """B x H_kv units of packed KV cache on one GPU (see module docstring)."""
+    """B x H_kv units of packed KV cache on one GPU: one reference
+    ``KvCacheState`` (kvcache.py:77-107) per unit, each with its own length.
+
+    Storage: K and V page pools (one 64-token chunk of one unit per page) on
+    CUDA virtual memory that grow without copying, a free list of page ids,
+    a page table [units][chunks], fp32 residual rows [units][64][128] and
+    per-unit chunk / residual counters on the device.  The host mirrors every
+    length (it issues every append), so an append is ONE kernel launch
+    (nsnkv_append: flushes, residual rows, page table and counters) with no
+    device->host synchronisation; page ids for newly flushed chunks come from
+    the free list and are uploaded with the launch only when a unit flushes.
+    Sequences end with ``release`` (pages return to the free list) and start
+    from reference snapshots with ``load_snapshot`` / ``import_unit``.
+    """
 
     def __init__(self, config: CacheConfig, batch: int, n_kv_heads: int, max_tokens: int = 0,
                  cb_k: Codebook | None = None, cb_v: Codebook | None = None,
@@ -205,71 +250,119 @@ class PagedKvCache:
         self.cb_k = cb_k
         self.cb_v = cb_v
         self.base_position = int(base_position)
-        self.total_tokens = 0
-        self.n_chunks = 0
-        self.n_res = 0
-        self.max_chunks = 0
-        dev = self.device
-        self.k_res = torch.zeros(self.units, R, D, dtype=torch.float32, device=dev)
-        self.v_res = torch.zeros(self.units, R, D, dtype=torch.float32, device=dev)
-        self.base_pos_t = torch.full((self.units,), self.base_position, dtype=torch.int64, device=dev)
-        self.k_pool = torch.zeros(0, self.page_bytes, dtype=torch.uint8, device=dev)
-        self.v_pool = torch.zeros(0, self.page_bytes, dtype=torch.uint8, device=dev)
-        self.page_table = torch.zeros(self.units, 0, dtype=torch.int32, device=dev)
-        self.k_counters = torch.zeros(self.units, 0, 4, dtype=torch.int32, device=dev)
-        self.v_counters = torch.zeros(self.units, 0, 4, dtype=torch.int32, device=dev)
-        self._n_chunks_t = torch.zeros(self.units, dtype=torch.int32, device=dev)
-        self._n_res_t = torch.zeros(self.units, dtype=torch.int32, device=dev)
+        U, dev = self.units, self.device
+        # host mirrors of the per-unit state (exact: every change goes through here)
+        self.unit_n_chunks = np.zeros(U, np.int64)
+        self.unit_n_res = np.zeros(U, np.int64)
+        self.unit_total = np.zeros(U, np.int64)
+        self.unit_base = np.full(U, self.base_position, np.int64)
+        self._pt = np.zeros((U, 0), np.int32)          # page table mirror
+        self._free = np.zeros(0, np.int32)              # free page ids (stack, top = end)
+        # device state
+        self.k_res = torch.zeros(U, R, D, dtype=torch.float32, device=dev)
+        self.v_res = torch.zeros(U, R, D, dtype=torch.float32, device=dev)
+        self._cnt = torch.zeros(2, 2, U, dtype=torch.int32, device=dev)  # [buf][chunks, res][unit]
+        self._cur = 0
+        self.base_pos_t = torch.full((U,), self.base_position, dtype=torch.int64, device=dev)
+        self.page_table = torch.zeros(U, 0, dtype=torch.int32, device=dev)
+        self._events = torch.zeros(0, 2, 4, dtype=torch.int32, device=dev)  # [page][K, V][counter]
+        self._pools = {"k": _Pool(dev, self.page_bytes), "v": _Pool(dev, self.page_bytes)}
         self._ws = torch.empty(0, dtype=torch.uint8, device=dev)
+        self._keep = []  # host buffers of in-flight uploads
         self.rope = RopeTable.get(dev, config.rope_base)
-        self._reserve_chunks((max_tokens + R - 1) // R)
+        if max_tokens:
+            self.reserve(max_tokens)
 
     # -- storage ------------------------------------------------------------
-    def _reserve_chunks(self, n: int) -> None:
-        """Grow the page pools so every unit can hold n chunks (pages of unit
-        u are u * max_chunks .. u * max_chunks + max_chunks - 1)."""
-        if n <= self.max_chunks:
+    @property
+    def capacity(self) -> int:
+        """Pages mapped in each pool."""
+        return self._events.shape[0]
+
+    def _grow_pages(self, need_free: int) -> None:
+        if self._free.size >= need_free:
             return
-        new = max(n, 2 * self.max_chunks)
-        dev = self.device
-        kp = torch.zeros(self.units * new, self.page_bytes, dtype=torch.uint8, device=dev)
-        vp = torch.zeros_like(kp)
-        kc = torch.zeros(self.units, new, 4, dtype=torch.int32, device=dev)
-        vc = torch.zeros_like(kc)
-        if self.max_chunks:
-            old = self.max_chunks
-            kp.view(self.units, new, -1)[:, :old].copy_(self.k_pool.view(self.units, old, -1))
-            vp.view(self.units, new, -1)[:, :old].copy_(self.v_pool.view(self.units, old, -1))
-            kc[:, :old].copy_(self.k_counters)
-            vc[:, :old].copy_(self.v_counters)
-        self.k_pool, self.v_pool, self.k_counters, self.v_counters = kp, vp, kc, vc
-        self.page_table = (torch.arange(self.units, device=dev, dtype=torch.int32)[:, None] * new
-                           + torch.arange(new, device=dev, dtype=torch.int32)[None, :]).contiguous()
-        self.max_chunks = new
+        old = self.capacity
+        want = old + (need_free - self._free.size)
+        want = max(want, old + old // 4, 64)
+        new = min(self._pools["k"].grow(want), self._pools["v"].grow(want))
+        ev = torch.zeros(new, 2, 4, dtype=torch.int32, device=self.device)
+        if old:
+            ev[:old].copy_(self._events)  # per-page event counters (32 B a page)
+        self._events = ev
+        # new ids pushed in descending order, so pops hand out ascending runs
+        self._free = np.concatenate([np.arange(new - 1, old - 1, -1, dtype=np.int32), self._free])
+
+    def _alloc(self, n: int) -> np.ndarray:
+        self._grow_pages(n)
+        ids = self._free[self._free.size - n:][::-1].copy()
+        self._free = self._free[:self._free.size - n]
+        return ids
+
+    def _ensure_width(self, chunks: int) -> None:
+        W = self._pt.shape[1]
+        if chunks <= W:
+            return
+        new = max(chunks, 2 * W, 16)
+        pt = np.zeros((self.units, new), np.int32)
+        pt[:, :W] = self._pt
+        self._pt = pt
+        t = torch.zeros(self.units, new, dtype=torch.int32, device=self.device)
+        if W:
+            t[:, :W].copy_(self.page_table)
+        self.page_table = t
 
     def reserve(self, max_tokens: int) -> "PagedKvCache":
-        """Pre-size the page pools and the RoPE table for contexts up to
-        max_tokens per unit, so later appends never grow them (a growth
-        reallocates and copies the pools: a server reserves up front)."""
+        """Pre-size pools, page table and RoPE table so every unit can hold
+        max_tokens tokens (a server reserves up front; growth later maps more
+        memory without copying pages)."""
         n = (int(max_tokens) + R - 1) // R
-        if n > self.max_chunks:
-            self._reserve_chunks(n)
-        self.rope.ensure(self.base_position + n * R)
+        need = int(np.maximum(n - self.unit_n_chunks, 0).sum())
+        self._grow_pages(need)
+        self._ensure_width(n)
+        self.rope.ensure(int(self.unit_base.max()) + n * R + R)
         return self
+
+    def pool_ptrs(self) -> tuple[int, int]:
+        return self._pools["k"].ptr, self._pools["v"].ptr
+
+    # -- lengths -------------------------------------------------------------
+    @property
+    def n_chunks(self) -> int:
+        """Flushed chunks (max over units; equal for uniform appends)."""
+        return int(self.unit_n_chunks.max())
+
+    @property
+    def n_res(self) -> int:
+        return int(self.unit_n_res.max())
+
+    @property
+    def total_tokens(self) -> int:
+        return int(self.unit_total.max())
 
     @property
     def n_quantized(self) -> int:
         return self.n_chunks * R
 
     @property
+    def max_chunks(self) -> int:
+        return self._pt.shape[1]
+
+    @property
     def max_tokens(self) -> int:
         """Row stride of score / weight buffers (a multiple of 64)."""
-        return max(R, (self.n_chunks + (1 if self.n_res else 0)) * R)
+        n = self.unit_n_chunks + (self.unit_n_res > 0)
+        return max(R, int(n.max()) * R)
 
     # -- append (kvcache.py:157-195) ------------------------------------------
     def append(self, keys, values, cb_k: Codebook | None = None,
-               cb_v: Codebook | None = None) -> "PagedKvCache":
-        """Append [B, H_kv, n, 128] keys (pre-RoPE) and values (post-HT)."""
+               cb_v: Codebook | None = None, seq_lens=None) -> "PagedKvCache":
+        """Append keys (pre-RoPE) and values (post-HT).
+
+        Uniform: [B, H_kv, n, 128] (every unit gains n tokens).  Ragged
+        (``seq_lens``, B ints): packed [sum(seq_lens), H_kv, 128], sequence b
+        contributing rows sum(seq_lens[:b]) .. + seq_lens[b] (zero = no
+        tokens this step).  One kernel launch either way."""
         cb_k = cb_k or self.cb_k
         cb_v = cb_v or self.cb_v
         if cb_k is None or cb_v is None:
@@ -277,51 +370,86 @@ class PagedKvCache:
         if cb_k.bit_mode != self.bit_mode or cb_v.bit_mode != self.bit_mode:
             raise ShapeMismatch("codebook bit mode does not match the cache")
         self.cb_k, self.cb_v = cb_k, cb_v
-        k = self._as_rows(keys)
-        v = self._as_rows(values)
-        if k.shape != v.shape:
-            raise ShapeMismatch("key and value batches must have the same shape")
+        U = self.units
+        if seq_lens is None:
+            k = self._as_rows(keys)
+            v = self._as_rows(values)
+            if k.shape != v.shape:
+                raise ShapeMismatch("key and value batches must have the same shape")
+            n = k.shape[1]
+            if n < 1:
+                raise ShapeMismatch("append needs at least one token")
+            n_new = np.full(U, n, np.int64)
+            counts_t = offs_t = None
+            row_stride = 1
+        else:
+            lens = np.asarray(seq_lens, np.int64).reshape(-1)
+            if lens.shape[0] != self.batch or (lens < 0).any():
+                raise ShapeMismatch(f"seq_lens must hold {self.batch} non-negative lengths")
+            k = self._as_packed(keys, int(lens.sum()))
+            v = self._as_packed(values, int(lens.sum()))
+            if k.shape != v.shape:
+                raise ShapeMismatch("key and value batches must have the same shape")
+            if not lens.any():
+                return self
+            H = self.n_kv_heads
+            cu = np.concatenate([[0], np.cumsum(lens)])
+            n_new = np.repeat(lens, H)
+            offs = (cu[:-1, None] * H + np.arange(H)[None, :]).reshape(-1)
+            counts_t = self._upload(n_new.astype(np.int32))
+            offs_t = self._upload(offs.astype(np.int64))
+            n = 0
+            row_stride = H
         if k.dtype != v.dtype:  # one fp32 / one bf16 batch: encode both from fp32
             k, v = k.float(), v.float()
-        n = k.shape[1]
-        if n < 1:
-            raise ShapeMismatch("append needs at least one token")
-        n_flush = (self.n_res + n) // R
-        if n_flush:
-            self._reserve_chunks(self.n_chunks + n_flush)
-            start = self.base_position + self.n_chunks * R
-            table = self.rope.ensure(start + n_flush * R)
-            page_ids = self.page_table[:, self.n_chunks:]
-            start_t = self._start_pos(start)
-            for is_key, rows, res, pool, cb, cnt in (
-                    (1, k, self.k_res, self.k_pool, cb_k, self.k_counters),
-                    (0, v, self.v_res, self.v_pool, cb_v, self.v_counters)):
-                cnt_view = cnt[:, self.n_chunks:self.n_chunks + n_flush]
-                cnt_buf = torch.empty(self.units, n_flush, 4, dtype=torch.int32, device=self.device)
-                _lib.check(_lib.lib.nsnkv_encode_chunks(
-                    res.data_ptr(), self.n_res, rows.data_ptr(),
-                    1 if rows.dtype == torch.bfloat16 else 0, n, self.units, n_flush,
-                    is_key, start_t.data_ptr(),
-                    table.data_ptr(), 0, table.shape[0], cb.device_handle(self.device),
-                    int(self.config.strategy), pool.data_ptr(), page_ids.data_ptr(),
-                    self.page_table.stride(0), cnt_buf.data_ptr(), _stream()))
-                cnt_view.copy_(cnt_buf)
-        # the residual keeps stream rows [n_flush * R, n_res + n)
-        consumed_fresh = n_flush * R - self.n_res if n_flush else 0
-        keep_from_res = 0 if n_flush else self.n_res
-        tail = n - consumed_fresh
-        if tail:
-            for rows, res in ((k, self.k_res), (v, self.v_res)):
-                res[:, keep_from_res:keep_from_res + tail].copy_(rows[:, consumed_fresh:])
-        self.n_res = keep_from_res + tail
-        self.n_chunks += n_flush
-        self.total_tokens += n
-        self._n_chunks_t.fill_(self.n_chunks)
-        self._n_res_t.fill_(self.n_res)
+        n_flush = (self.unit_n_res + n_new) // R
+        fmax = int(n_flush.max())
+        new_pages_t = None
+        if fmax:
+            self._ensure_width(int((self.unit_n_chunks + n_flush).max()))
+            ids = self._alloc(int(n_flush.sum()))
+            npg = np.zeros((U, fmax), np.int32)
+            pos = 0
+            for u in np.nonzero(n_flush)[0]:
+                f = int(n_flush[u])
+                npg[u, :f] = ids[pos:pos + f]
+                self._pt[u, self.unit_n_chunks[u]:self.unit_n_chunks[u] + f] = ids[pos:pos + f]
+                pos += f
+            new_pages_t = self._upload(npg)
+        table = self.rope.ensure(int((self.unit_base + (self.unit_n_chunks + n_flush) * R).max()) + R)
+        a = _lib.AppendArgs()
+        a.n_units, a.max_flush = U, fmax
+        a.fresh_k, a.fresh_v = k.data_ptr(), v.data_ptr()
+        a.fresh_bf16 = 1 if k.dtype == torch.bfloat16 else 0
+        a.n_new_uniform = n
+        a.new_count = counts_t.data_ptr() if counts_t is not None else None
+        a.fresh_off = offs_t.data_ptr() if offs_t is not None else None
+        a.fresh_row_stride = row_stride
+        a.k_res, a.v_res = self.k_res.data_ptr(), self.v_res.data_ptr()
+        src, dst = self._cnt[self._cur], self._cnt[1 - self._cur]
+        a.n_chunks_in, a.n_res_in = src[0].data_ptr(), src[1].data_ptr()
+        a.n_chunks_out, a.n_res_out = dst[0].data_ptr(), dst[1].data_ptr()
+        a.base_pos = self.base_pos_t.data_ptr()
+        a.page_table = self.page_table.data_ptr() if self.page_table.numel() else None
+        a.page_table_stride = self.page_table.stride(0) if self.page_table.numel() else 0
+        a.new_pages = new_pages_t.data_ptr() if new_pages_t is not None else None
+        a.k_pool, a.v_pool = self.pool_ptrs()
+        a.counters = self._events.data_ptr() if self._events.numel() else None
+        a.rope_cs, a.rope_pos0, a.rope_n = table.data_ptr(), 0, table.shape[0]
+        a.cb_k, a.cb_v = cb_k.device_handle(self.device), cb_v.device_handle(self.device)
+        a.strategy = int(self.config.strategy)
+        _lib.check(_lib.lib.nsnkv_append(ctypes.byref(a), _stream()))
+        self._keep = [k, v]  # fresh rows stay alive until the next append is enqueued
+        self._cur = 1 - self._cur
+        self.unit_n_chunks += n_flush
+        self.unit_n_res = self.unit_n_res + n_new - n_flush * R
+        self.unit_total += n_new
         return self
 
-    def _start_pos(self, start: int) -> torch.Tensor:
-        return torch.full((self.units,), start, dtype=torch.int64, device=self.device)
+    def _upload(self, arr: np.ndarray) -> torch.Tensor:
+        """Host array -> device tensor without a host sync (pinned staging)."""
+        h = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+        return h.to(self.device, non_blocking=True)
 
     def _as_rows(self, x) -> torch.Tensor:
         if isinstance(x, np.ndarray):
@@ -336,12 +464,121 @@ class PagedKvCache:
             x = x.reshape(self.units, x.shape[2], x.shape[3])
         if x.dim() != 3 or x.shape[0] != self.units or x.shape[2] != D:
             raise ShapeMismatch(f"expected rows of {D} channels for {self.units} units, got {tuple(x.shape)}")
+        return self._device_rows(x)
+
+    def _as_packed(self, x, rows: int) -> torch.Tensor:
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        if (not torch.is_tensor(x) or x.dim() != 3 or x.shape[0] != rows
+                or x.shape[1] != self.n_kv_heads or x.shape[2] != D):
+            raise ShapeMismatch(f"expected packed [{rows}, {self.n_kv_heads}, {D}] rows")
+        return self._device_rows(x)
+
+    def _device_rows(self, x: torch.Tensor) -> torch.Tensor:
         if x.dtype not in (torch.float32, torch.bfloat16):
             x = x.float()
         x = x.to(self.device, non_blocking=True).contiguous()
         if self.check_finite and x.numel() and not bool(torch.isfinite(x).all()):
             raise ValueError("tensor contains NaN or Inf")
         return x
+
+    # -- sequence lifecycle ------------------------------------------------------
+    def _units_of(self, seqs) -> np.ndarray:
+        b = np.asarray(seqs, np.int64).reshape(-1)
+        if ((b < 0) | (b >= self.batch)).any():
+            raise IndexOutOfRange("sequence index out of range")
+        return (b[:, None] * self.n_kv_heads + np.arange(self.n_kv_heads)[None, :]).reshape(-1)
+
+    def release(self, seqs, base_position: int = 0) -> "PagedKvCache":
+        """End sequences: their pages go back to the free list and their units
+        start empty at ``base_position`` (the slot can take a new sequence)."""
+        units = self._units_of(seqs)
+        for u in units:
+            n = int(self.unit_n_chunks[u])
+            if n:
+                self._free = np.concatenate([self._free, self._pt[u, :n][::-1]])
+        self.unit_n_chunks[units] = 0
+        self.unit_n_res[units] = 0
+        self.unit_total[units] = 0
+        self.unit_base[units] = int(base_position)
+        ut = torch.from_numpy(units).to(self.device)
+        self._cnt[self._cur][:, ut] = 0
+        self.base_pos_t[ut] = int(base_position)
+        return self
+
+    def import_unit(self, unit: int, k_wire, v_wire, k_res=None, v_res=None,
+                    base_position: int | None = None) -> "PagedKvCache":
+        """Load one reference ``KvCacheState`` into an empty unit: serialized
+        chunks (vq.py:363-380, deserialize_chunk vq.py:383-428) become pages,
+        the residual rows (keys pre-RoPE, values post-HT) are copied in."""
+        u = int(unit)
+        if not 0 <= u < self.units:
+            raise IndexOutOfRange("unit out of range")
+        if self.unit_total[u]:
+            raise ShapeMismatch("import_unit needs an empty unit (release it first)")
+        kw, vw = list(k_wire), list(v_wire)
+        if len(kw) != len(vw):
+            raise ShapeMismatch("key and value chunk counts differ")
+        n = len(kw)
+        kr = np.zeros((0, D), np.float32) if k_res is None else np.array(k_res, np.float32).reshape(-1, D)
+        vr = np.zeros((0, D), np.float32) if v_res is None else np.array(v_res, np.float32).reshape(-1, D)
+        if kr.shape != vr.shape or kr.shape[0] >= R:
+            raise ShapeMismatch("residual rows must be [< 64, 128] for keys and values alike")
+        for blob in kw + vw:
+            _n, _d, bm, strat = struct.unpack_from("<HHBB", bytes(blob), 0)
+            if bm != int(self.bit_mode) or strat != int(self.config.strategy):
+                raise FormatError("chunk bit mode / strategy does not match the cache")
+        if base_position is not None:
+            self.unit_base[u] = int(base_position)
+            self.base_pos_t[u] = int(base_position)
+        if n:
+            ids = self._alloc(n)
+            self._ensure_width(n)
+            self._pt[u, :n] = ids
+            for kind, blobs in (("k", kw), ("v", vw)):
+                pages = np.stack([wire_to_page(bytes(b), kind) for b in blobs])
+                _lib.check(_lib.lib.nsnkv_pages_copy(self._pools[kind].ptr, self.page_bytes,
+                                                     ids.ctypes.data, n, pages.ctypes.data, 1, _stream()))
+            self.page_table[u, :n] = torch.from_numpy(ids).to(self.device)
+            self._events[torch.from_numpy(ids.astype(np.int64)).to(self.device)] = 0
+            torch.cuda.current_stream(self.device).synchronize()  # host page buffers
+        m = kr.shape[0]
+        if m:
+            self.k_res[u, :m] = torch.from_numpy(kr).to(self.device)
+            self.v_res[u, :m] = torch.from_numpy(vr).to(self.device)
+        self._cnt[self._cur, 0, u] = n
+        self._cnt[self._cur, 1, u] = m
+        self.unit_n_chunks[u], self.unit_n_res[u], self.unit_total[u] = n, m, n * R + m
+        self.rope.ensure(int(self.unit_base[u]) + n * R + R)
+        return self
+
+    def load_snapshot(self, unit: int, blob: bytes) -> "PagedKvCache":
+        """Inverse of ``snapshot`` / the reference kvcache.snapshot byte image
+        (kvcache.py:198-213)."""
+        b = bytes(blob)
+        if b[:4] != b"NSNS":
+            raise FormatError("bad snapshot: missing magic")
+        n, total, base = struct.unpack_from("<IQQ", b, 4)
+        pos = 24
+        blobs = []
+        for _ in range(2 * n):
+            (ln,) = struct.unpack_from("<I", b, pos)
+            blobs.append(b[pos + 4:pos + 4 + ln])
+            pos += 4 + ln
+        res = []
+        for _ in range(2):
+            (ln,) = struct.unpack_from("<I", b, pos)
+            t = b[pos + 4:pos + 4 + ln]
+            pos += 4 + ln
+            if t[:4] != b"NSNT":
+                raise FormatError("bad snapshot: residual tensor")
+            rows, cols = struct.unpack_from("<II", t, 4)
+            res.append(np.frombuffer(t, "<f4", rows * cols, 12).reshape(rows, cols))
+        if pos != len(b):
+            raise FormatError("bad snapshot: trailing bytes")
+        if total != n * R + res[0].shape[0]:
+            raise FormatError("bad snapshot: token count")
+        return self.import_unit(unit, blobs[:n], blobs[n:], res[0], res[1], base_position=base)
 
     # -- decode ----------------------------------------------------------------
     def view(self, n_q_heads: int, cb_k: Codebook | None = None,
@@ -352,16 +589,16 @@ class PagedKvCache:
             raise ShapeMismatch("decode needs the key and value codebooks")
         if n_q_heads % self.n_kv_heads:
             raise ShapeMismatch("n_q_heads must be a multiple of n_kv_heads")
-        table = self.rope.ensure(self.base_position + self.n_chunks * R + R)
+        table = self.rope.ensure(int((self.unit_base + self.unit_n_chunks * R).max()) + R)
+        cnt = self._cnt[self._cur]
         cv = _lib.CacheView()
-        cv.k_pool = self.k_pool.data_ptr()
-        cv.v_pool = self.v_pool.data_ptr()
-        cv.page_table = self.page_table.data_ptr()
-        cv.page_table_stride = self.page_table.stride(0)
-        cv.n_chunks = self._n_chunks_t.data_ptr()
+        cv.k_pool, cv.v_pool = self.pool_ptrs()
+        cv.page_table = self.page_table.data_ptr() if self.page_table.numel() else None
+        cv.page_table_stride = self.page_table.stride(0) if self.page_table.numel() else 0
+        cv.n_chunks = cnt[0].data_ptr()
         cv.k_res = self.k_res.data_ptr()
         cv.v_res = self.v_res.data_ptr()
-        cv.n_res = self._n_res_t.data_ptr()
+        cv.n_res = cnt[1].data_ptr()
         cv.base_pos = self.base_pos_t.data_ptr()
         cv.batch = self.batch
         cv.n_kv_heads = self.n_kv_heads
@@ -372,7 +609,7 @@ class PagedKvCache:
         cv.rope_n = table.shape[0]
         cv.cb_k = cb_k.device_handle(self.device)
         cv.cb_v = cb_v.device_handle(self.device)
-        cv.total_chunks = self.units * self.n_chunks
+        cv.total_chunks = int(self.unit_n_chunks.sum())
         cv.precision = PRECISIONS[self.precision]
         return cv
 
@@ -423,9 +660,17 @@ class PagedKvCache:
 
     def attend(self, q, out: torch.Tensor | None = None, lse: torch.Tensor | None = None) -> torch.Tensor:
         """Fused softmax(q.K^T / sqrt(d)) . V -> [B, Hq, 128] (attention.py:136-142)."""
-        q = self._q(q)
         if self.total_tokens == 0:
             raise ShapeMismatch("attention over an empty cache")
+        q, cv, out = self._attend_args(q, out, lse)
+        ws = self._workspace(cv)
+        _lib.check(_lib.lib.nsnkv_decode_attend(cv, q.data_ptr(), out.data_ptr(),
+                                                lse.data_ptr() if lse is not None else None,
+                                                ws.data_ptr(), ws.numel(), _stream()))
+        return out
+
+    def _attend_args(self, q, out, lse):
+        q = self._q(q)
         cv = self.view(q.shape[1])
         rows = self.batch * q.shape[1]
         if out is None:
@@ -438,24 +683,71 @@ class PagedKvCache:
                     or t.numel() != n):
                 raise ShapeMismatch(f"{name} must be a contiguous float32 tensor of {n} elements "
                                     f"on {self.device}, got {t.dtype} {tuple(t.shape)} on {t.device}")
+        return q, cv, out
+
+    def decode_step(self, q, keys, values, out: torch.Tensor | None = None,
+                    lse: torch.Tensor | None = None) -> torch.Tensor:
+        """One serving decode step: append [B, H_kv, n, 128] keys / values
+        (n >= 1, usually 1) to every sequence, then attend q over the cache
+        including them (kvcache.append + attend_quantized).  When no unit
+        completes a chunk this is the attend launches alone (the combine
+        kernel attends the new rows as residual rows and stores them); a step
+        that completes a chunk runs nsnkv_append first."""
+        k = self._as_rows(keys)
+        v = self._as_rows(values)
+        if k.shape != v.shape:
+            raise ShapeMismatch("key and value batches must have the same shape")
+        n = k.shape[1]
+        if n < 1 or int((self.unit_n_res + n).max()) >= R:
+            self.append(k, v)
+            return self.attend(q, out=out, lse=lse)
+        if k.dtype != v.dtype:
+            k, v = k.float(), v.float()
+        q, cv, out = self._attend_args(q, out, lse)
         ws = self._workspace(cv)
-        _lib.check(_lib.lib.nsnkv_decode_attend(cv, q.data_ptr(), out.data_ptr(),
-                                                lse.data_ptr() if lse is not None else None,
-                                                ws.data_ptr(), ws.numel(), _stream()))
+        _lib.check(_lib.lib.nsnkv_decode_step(
+            cv, q.data_ptr(), k.data_ptr(), v.data_ptr(), 1 if k.dtype == torch.bfloat16 else 0, n,
+            self._cnt[self._cur][1].data_ptr(), out.data_ptr(),
+            lse.data_ptr() if lse is not None else None, ws.data_ptr(), ws.numel(), _stream()))
+        self._keep = [k, v]
+        self.unit_n_res += n
+        self.unit_total += n
         return out
 
     # -- counters (kvcache.py:86-88, 191-194) ---------------------------------
     def counters(self) -> np.ndarray:
         """Per-unit [clamp, zero_vector, s3_fallback, near_tie] event totals."""
-        k = self.k_counters[:, :self.n_chunks].sum(dim=1)
-        v = self.v_counters[:, :self.n_chunks].sum(dim=1)
-        return (k + v).cpu().numpy().astype(np.int64)
+        ev = self._events.sum(dim=1).cpu().numpy().astype(np.int64)  # [page][4], K + V
+        out = np.zeros((self.units, 4), np.int64)
+        for u in range(self.units):
+            n = int(self.unit_n_chunks[u])
+            if n:
+                out[u] = ev[self._pt[u, :n]].sum(axis=0)
+        return out
 
     # -- export: pages -> reference wire format (vq.py:363-380) ---------------
     def pages(self, unit: int, kind: str = "k") -> np.ndarray:
-        pool = self.k_pool if kind == "k" else self.v_pool
-        ids = self.page_table[unit, :self.n_chunks].long()
-        return pool[ids].cpu().numpy()
+        """[n_chunks, page_bytes] device pages of one unit (host copy)."""
+        n = int(self.unit_n_chunks[unit])
+        out = np.empty((n, self.page_bytes), np.uint8)
+        if n:
+            ids = np.ascontiguousarray(self._pt[unit, :n])
+            _lib.check(_lib.lib.nsnkv_pages_copy(self._pools[kind].ptr, self.page_bytes,
+                                                 ids.ctypes.data, n, out.ctypes.data, 0, _stream()))
+            torch.cuda.current_stream(self.device).synchronize()
+        return out
+
+    def all_pages(self, kind: str = "k") -> np.ndarray:
+        """Pages of every unit, unit-major ([sum n_chunks, page_bytes])."""
+        ids = np.concatenate([self._pt[u, :self.unit_n_chunks[u]] for u in range(self.units)]
+                             ).astype(np.int32)
+        out = np.empty((ids.size, self.page_bytes), np.uint8)
+        if ids.size:
+            _lib.check(_lib.lib.nsnkv_pages_copy(self._pools[kind].ptr, self.page_bytes,
+                                                 ids.ctypes.data, ids.size, out.ctypes.data, 0,
+                                                 _stream()))
+            torch.cuda.current_stream(self.device).synchronize()
+        return out
 
     def wire_chunks(self, unit: int, kind: str = "k") -> np.ndarray:
         """[n_chunks, wire_bytes] reference serialized chunks of one unit."""
@@ -466,13 +758,14 @@ class PagedKvCache:
 
     def snapshot(self, unit: int = 0) -> bytes:
         """kvcache.snapshot byte image of one unit (kvcache.py:198-213)."""
+        n, m = int(self.unit_n_chunks[unit]), int(self.unit_n_res[unit])
         out = bytearray(b"NSNS")
-        out += struct.pack("<IQQ", self.n_chunks, self.total_tokens, self.base_position)
+        out += struct.pack("<IQQ", n, int(self.unit_total[unit]), int(self.unit_base[unit]))
         for kind in ("k", "v"):
             for blob in self.chunk_wire(unit, kind):
                 out += struct.pack("<I", len(blob)) + blob
         for res in (self.k_res, self.v_res):
-            rows = res[unit, :self.n_res].cpu().numpy().astype("<f4")
+            rows = res[unit, :m].cpu().numpy().astype("<f4")
             blob = b"NSNT" + struct.pack("<II", rows.shape[0], D) + rows.tobytes()
             out += struct.pack("<I", len(blob)) + blob
         return bytes(out)

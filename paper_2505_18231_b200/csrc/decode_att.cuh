@@ -168,47 +168,97 @@ __device__ __forceinline__ int k_channel(int t, int kt, int r, int i) {
 // ---------------------------------------------------------------------------
 // combine: merge the stream-K records of a unit with its exact residual rows,
 // normalise, inverse FWHT (attention.py:105-108, 129-133, 141).
-// One warp per (batch, q-head); lane l owns channels 4l .. 4l+3.
+// One CTA (256 threads) per unit; warp h < G owns q-head h of the unit.
+//
+// Residual rows are staged once per unit: keys rotated to their positions
+// (rope.py:35-51) into kr, values into vr, by all 256 threads with
+// independent loads; each warp then scores its head's rows (lane = row) and
+// accumulates the weighted value rows (lane = 4 channels).
+//
+// Fused append (nsnkv_decode_step): n_new > 0 extra rows per unit come from
+// new_k / new_v ([units][n_new][128], fp32 or bf16) -- attended as residual
+// rows nres .. nres + n_new - 1 and written into the residual buffer, with
+// the unit's residual count published to n_res_out (which may be cv.n_res
+// itself: one CTA owns the unit and reads the count before it writes it).
 // ---------------------------------------------------------------------------
-constexpr int COMBINE_ROWS = 4;  // warps (rows) per CTA
+constexpr int COMBINE_THREADS = 256;
 
-// ALLREC: every group wrote a record for every unit its CTA touches (m = -inf
-// when it saw none of the unit's chunks), so no ownership test is needed.
+struct CombineSmem {
+  float kr[R][D + 1];  // rotated residual keys (row stride D + 1: lane = row is conflict-free)
+  __align__(16) float vr[R][D];
+  __align__(16) float q[8][D];
+  float w[8][R];
+};
+
 template <int G, int NGRP, bool ALLREC = false>
-__global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
+__global__ void __launch_bounds__(COMBINE_THREADS) combine_kernel(
     CacheViewDev cv, const float *__restrict__ qg, const float *__restrict__ recs,
-    int64_t total_chunks, int grid, float *__restrict__ out, float *__restrict__ lse) {
-  __shared__ __align__(16) float s_q[COMBINE_ROWS][D];
-  __shared__ float s_w[COMBINE_ROWS][R];
-  // G >= COMBINE_ROWS: the CTA's rows are q-heads of one unit, so the rotated
-  // residual keys are staged once per CTA (row stride D + 1: conflict-free
-  // when lane t reads row t)
-  constexpr bool SHARED_RES = G >= COMBINE_ROWS;
-  __shared__ float s_kr[SHARED_RES ? R : 1][D + 1];
-  const int wr = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * COMBINE_ROWS + wr;
-  if (row >= cv.batch * cv.n_q_heads) return;
-  const int b = row / cv.n_q_heads, i = row - b * cv.n_q_heads;
-  const int hk = i / G, h = i - hk * G;
-  const int u = b * cv.n_kv_heads + hk;
-  int64_t off = 0;  // global chunk offset of unit u
-  for (int uu = lane; uu < u; uu += 32) off += cv.n_chunks[uu];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
-  const float4 q4 = *reinterpret_cast<const float4 *>(qg + (int64_t)row * D + 4 * lane);
-  *reinterpret_cast<float4 *>(&s_q[wr][4 * lane]) = q4;
+    int64_t total_chunks, int grid, float *__restrict__ out, float *__restrict__ lse,
+    const void *__restrict__ new_k, const void *__restrict__ new_v, int new_bf16, int n_new,
+    int32_t *__restrict__ n_res_out) {
+  extern __shared__ __align__(16) unsigned char combine_smem[];
+  CombineSmem &S = *reinterpret_cast<CombineSmem *>(combine_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x;
+  const int b = u / cv.n_kv_heads, hk = u - b * cv.n_kv_heads;
   const int nch = cv.n_chunks[u];
-  float m = -INFINITY, l = 0.f;
+  const int nres = cv.n_res[u];
+  const int rtot = nres + n_new;
+  const int64_t pbase = cv.base_pos[u] + (int64_t)nch * R;
+
+  // ---- stage the residual rows (old from the buffer, new from the input) --
+  for (int i = threadIdx.x; i < rtot * (D / 4); i += COMBINE_THREADS) {
+    const int tt = i / (D / 4), l4 = i - tt * (D / 4);
+    float4 k4, v4;
+    if (tt < nres) {
+      k4 = *reinterpret_cast<const float4 *>(cv.k_res + ((int64_t)u * R + tt) * D + 4 * l4);
+      v4 = *reinterpret_cast<const float4 *>(cv.v_res + ((int64_t)u * R + tt) * D + 4 * l4);
+    } else {
+      const int64_t off = ((int64_t)u * n_new + (tt - nres)) * D + 4 * l4;
+      if (new_bf16) {
+        const uint2 rk = *reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(new_k) + off);
+        const uint2 rv = *reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(new_v) + off);
+        k4 = make_float4(bf16_to_f32(rk.x & 0xffffu), bf16_to_f32(rk.x >> 16),
+                         bf16_to_f32(rk.y & 0xffffu), bf16_to_f32(rk.y >> 16));
+        v4 = make_float4(bf16_to_f32(rv.x & 0xffffu), bf16_to_f32(rv.x >> 16),
+                         bf16_to_f32(rv.y & 0xffffu), bf16_to_f32(rv.y >> 16));
+      } else {
+        k4 = *reinterpret_cast<const float4 *>(static_cast<const float *>(new_k) + off);
+        v4 = *reinterpret_cast<const float4 *>(static_cast<const float *>(new_v) + off);
+      }
+      // the new rows join the residual buffer (keys pre-RoPE, values post-HT)
+      *reinterpret_cast<float4 *>(const_cast<float *>(cv.k_res) + ((int64_t)u * R + tt) * D + 4 * l4) = k4;
+      *reinterpret_cast<float4 *>(const_cast<float *>(cv.v_res) + ((int64_t)u * R + tt) * D + 4 * l4) = v4;
+    }
+    const float4 c4 = *reinterpret_cast<const float4 *>(cv.rope_cs + (pbase + tt - cv.rope_pos0) * NPAIR + 2 * l4);
+    float *kr = &S.kr[tt][4 * l4];
+    kr[0] = k4.x * c4.x - k4.y * c4.y;
+    kr[1] = k4.x * c4.y + k4.y * c4.x;
+    kr[2] = k4.z * c4.z - k4.w * c4.w;
+    kr[3] = k4.z * c4.w + k4.w * c4.z;
+    *reinterpret_cast<float4 *>(&S.vr[tt][4 * l4]) = v4;
+  }
+  const int h = warp;
+  const bool active = h < G;
+  const int row = b * cv.n_q_heads + hk * G + h;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (nch > 0) {
-    const int64_t x0 = off, x1 = off + nch - 1;
-    int c0 = (int)(x0 * grid / total_chunks);
-    while (c0 + 1 < grid && range_lo(total_chunks, c0 + 1, grid) <= x0) ++c0;
-    while (c0 > 0 && range_lo(total_chunks, c0, grid) > x0) --c0;
-    int c1 = (int)(x1 * grid / total_chunks);
-    while (c1 + 1 < grid && range_lo(total_chunks, c1 + 1, grid) <= x1) ++c1;
-    while (c1 > 0 && range_lo(total_chunks, c1, grid) > x1) --c1;
-    if (ALLREC) {
+  float m = -INFINITY, l = 0.f;
+  if (active) {
+    *reinterpret_cast<float4 *>(&S.q[h][4 * lane]) =
+        *reinterpret_cast<const float4 *>(qg + (int64_t)row * D + 4 * lane);
+    // ---- stream-K records of the unit -----------------------------------
+    int64_t off = 0;  // global chunk offset of unit u
+    for (int uu = lane; uu < u; uu += 32) off += cv.n_chunks[uu];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+    if (nch > 0) {
+      const int64_t x0 = off, x1 = off + nch - 1;
+      int c0 = (int)(x0 * grid / total_chunks);
+      while (c0 + 1 < grid && range_lo(total_chunks, c0 + 1, grid) <= x0) ++c0;
+      while (c0 > 0 && range_lo(total_chunks, c0, grid) > x0) --c0;
+      int c1 = (int)(x1 * grid / total_chunks);
+      while (c1 + 1 < grid && range_lo(total_chunks, c1 + 1, grid) <= x1) ++c1;
+      while (c1 > 0 && range_lo(total_chunks, c1, grid) > x1) --c1;
       // every (CTA, group) slot of the unit holds a record (m = -inf when
       // empty): load them in batches of 8 with independent loads, then merge
       const int nrec = (c1 - c0 + 1) * NGRP;
@@ -245,97 +295,33 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
           m = mn;
         }
       }
-    } else
-    for (int c = c0; c <= c1; ++c) {
-      // local chunk indices of unit u inside CTA c; group gq owns k % NGRP == gq
-      const int64_t clo = range_lo(total_chunks, c, grid);
-      const int64_t chi = range_lo(total_chunks, c + 1, grid);
-      const int64_t ka = (x0 > clo ? x0 : clo) - clo;
-      const int64_t kb = (x1 + 1 < chi ? x1 + 1 : chi) - clo;
-      for (int gq = 0; gq < NGRP; ++gq) {
-        if (!ALLREC && !(ka + ((gq - ka % NGRP + NGRP) % NGRP) < kb)) continue;
-        const float *rec = record_ptr<G>(const_cast<float *>(recs), (u + c) * NGRP + gq) + h * (4 + D);
-        const float rm = rec[0], rl = rec[1];
-        if (!(rm > -INFINITY)) continue;  // the group saw no chunk of this unit
-        const float mn = fmaxf(m, rm);
-        const float sa = exp2f(m - mn), sb = exp2f(rm - mn);
-        const float4 r4 = *reinterpret_cast<const float4 *>(rec + 4 + 4 * lane);
-        a.x = a.x * sa + r4.x * sb;
-        a.y = a.y * sa + r4.y * sb;
-        a.z = a.z * sa + r4.z * sb;
-        a.w = a.w * sa + r4.w * sb;
-        l = l * sa + rl * sb;
-        m = mn;
-      }
     }
   }
-  __syncwarp();
-  // residual rows: exact RoPE(k, pos) . q scores (base-2 logits)
-  const int nres = cv.n_res[u];
-  if (nres > 0) {
-    const int64_t pbase = cv.base_pos[u] + (int64_t)nch * R;
-    if constexpr (SHARED_RES) {
-      // every thread of the CTA rotates a share of the rows (coalesced loads,
-      // all in flight together), then lane t scores row t against its q-head
-      for (int idx = threadIdx.x; idx < nres * (D / 4); idx += 32 * COMBINE_ROWS) {
-        const int tt = idx / (D / 4), l4 = idx - tt * (D / 4);
-        const float4 k4 = *reinterpret_cast<const float4 *>(cv.k_res + ((int64_t)u * R + tt) * D + 4 * l4);
-        const float4 c4 = *reinterpret_cast<const float4 *>(
-            cv.rope_cs + (pbase + tt - cv.rope_pos0) * NPAIR + 2 * l4);
-        float *kr = &s_kr[tt][4 * l4];
-        kr[0] = k4.x * c4.x - k4.y * c4.y;
-        kr[1] = k4.x * c4.y + k4.y * c4.x;
-        kr[2] = k4.z * c4.z - k4.w * c4.w;
-        kr[3] = k4.z * c4.w + k4.w * c4.z;
-      }
-      __syncthreads();
-      for (int tt = lane; tt < nres; tt += 32) {
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};  // four independent chains
+  __syncthreads();  // staged rows and q visible; every thread has read n_res[u]
+  if (n_new > 0 && n_res_out && threadIdx.x == 0) n_res_out[u] = rtot;  // may alias cv.n_res
+  if (active && rtot > 0) {
+    // ---- residual rows: exact RoPE(k, pos) . q scores (base-2 logits) ----
+    for (int tt = lane; tt < rtot; tt += 32) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};  // four independent chains
 #pragma unroll 8
-        for (int d = 0; d < D; d += 4)
+      for (int d = 0; d < D; d += 4)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc[e] = fmaf(s_kr[tt][d + e], s_q[wr][d + e], acc[e]);
-        s_w[wr][tt] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * LOG2E_OVER_SQRTD;
-      }
-    } else {
-    // warp-cooperative: lane l rotates and multiplies channels 4l .. 4l+3
-    // (pairs 2l, 2l+1) of 8 rows at a time (coalesced row loads), then one
-    // butterfly per row
-    for (int t0 = 0; t0 < nres; t0 += 8) {
-      float part[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        part[i] = 0.f;
-        const int tt = t0 + i;
-        if (tt < nres) {
-          const float4 k4 = *reinterpret_cast<const float4 *>(cv.k_res + ((int64_t)u * R + tt) * D + 4 * lane);
-          const float4 c4 = *reinterpret_cast<const float4 *>(
-              cv.rope_cs + (pbase + tt - cv.rope_pos0) * NPAIR + 2 * lane);
-          const float re0 = k4.x * c4.x - k4.y * c4.y, ro0 = k4.x * c4.y + k4.y * c4.x;
-          const float re1 = k4.z * c4.z - k4.w * c4.w, ro1 = k4.z * c4.w + k4.w * c4.z;
-          part[i] = fmaf(ro1, q4.w, fmaf(re1, q4.z, fmaf(ro0, q4.y, re0 * q4.x)));
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) part[i] += __shfl_xor_sync(0xffffffffu, part[i], o);
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (lane == i && t0 + i < nres) s_w[wr][t0 + i] = part[i] * LOG2E_OVER_SQRTD;
-    }
+        for (int e = 0; e < 4; ++e) acc[e] = fmaf(S.kr[tt][d + e], S.q[h][d + e], acc[e]);
+      S.w[h][tt] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * LOG2E_OVER_SQRTD;
     }
     __syncwarp();
     float rm = -INFINITY;
-    for (int tt = 0; tt < nres; ++tt) rm = fmaxf(rm, s_w[wr][tt]);
+    for (int tt = lane; tt < rtot; tt += 32) rm = fmaxf(rm, S.w[h][tt]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rm = fmaxf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
     const float mn = fmaxf(m, rm);
     const float sa = (m > -INFINITY) ? exp2f(m - mn) : 0.f;
     a.x *= sa; a.y *= sa; a.z *= sa; a.w *= sa;
     l *= sa;
-#pragma unroll 8
-    for (int tt = 0; tt < nres; ++tt) {
-      const float p = exp2f(s_w[wr][tt] - mn);
-      const float4 v4 = *reinterpret_cast<const float4 *>(cv.v_res + ((int64_t)u * R + tt) * D + 4 * lane);
+#pragma unroll 4
+    for (int tt = 0; tt < rtot; ++tt) {
+      const float p = exp2f(S.w[h][tt] - mn);
+      const float4 v4 = *reinterpret_cast<const float4 *>(&S.vr[tt][4 * lane]);
       l += p;
       a.x = fmaf(p, v4.x, a.x);
       a.y = fmaf(p, v4.y, a.y);
@@ -344,6 +330,7 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
     }
     m = mn;
   }
+  if (!active) return;
   const float inv = (l > 0.f) ? 1.f / l : 0.f;
   float4 v = make_float4(a.x * inv, a.y * inv, a.z * inv, a.w * inv);
   // inverse FWHT in the warp (stages h = 1, 2 in-lane, 4 .. 64 by shuffles)
@@ -373,7 +360,16 @@ __global__ void __launch_bounds__(32 * COMBINE_ROWS) combine_kernel(
 
 
 
+// rows appended to every unit's residual by the decode step itself
+// (nsnkv_decode_step); n == 0 for plain attention
+struct AppendRows {
+  const void *k = nullptr, *v = nullptr;
+  int bf16 = 0, n = 0;
+  int32_t *n_res_out = nullptr;
+};
+
 // warp-specialized decode launcher (decode_attend3.cu), G = 1, 2, 4, 8
 template <int G, bool FOLD, int PREC>
 int nsnkv_launch_attend3(const nsnkv::CacheViewDev &cv, const float *q, float *out, float *lse,
-                         float *recs, int64_t total, int grid, cudaStream_t st);
+                         float *recs, int64_t total, int grid, cudaStream_t st,
+                         const AppendRows &add);

@@ -1012,17 +1012,19 @@ using namespace nsnkv;
 
 template <int G, bool FOLD, int PREC>
 int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, float *lse,
-                         float *recs, int64_t total, int grid, cudaStream_t st) {
-  static unsigned long long attr = 0;
+                         float *recs, int64_t total, int grid, cudaStream_t st,
+                         const AppendRows &add) {
+  static unsigned long long attr = 0, attr_c = 0;
   set_smem_attr_once(attend3_kernel<G, FOLD, PREC>, ATT_SMEM_BYTES, attr);
+  set_smem_attr_once(combine_kernel<G, 3, true>, (int)sizeof(CombineSmem), attr_c);
   int launches = 0;
   if (total > 0) {
     attend3_kernel<G, FOLD, PREC><<<grid, 512, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
     ++launches;
   }
-  combine_kernel<G, 3, true>
-      <<<(cv.batch * cv.n_q_heads + COMBINE_ROWS - 1) / COMBINE_ROWS, 32 * COMBINE_ROWS, 0, st>>>(
-          cv, q, recs, total > 0 ? total : 1, grid, out, lse);
+  combine_kernel<G, 3, true><<<cv.batch * cv.n_kv_heads, COMBINE_THREADS, sizeof(CombineSmem), st>>>(
+      cv, q, recs, total > 0 ? total : 1, grid, out, lse, add.k, add.v, add.bf16, add.n,
+      add.n_res_out);
   ++launches;
   nsnkv_internal_count_launch(launches);
   return nsnkv_internal_check_launch("decode_attend");
@@ -1030,7 +1032,8 @@ int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, flo
 
 #define NSNKV_A3_INST(GG, FF, PP)                                                            \
   template int nsnkv_launch_attend3<GG, FF, PP>(const CacheViewDev &, const float *, float *, \
-                                                float *, float *, int64_t, int, cudaStream_t);
+                                                float *, float *, int64_t, int, cudaStream_t,    \
+                                                const AppendRows &);
 #define NSNKV_A3_INST_G(GG) \
   NSNKV_A3_INST(GG, true, 0) NSNKV_A3_INST(GG, true, 1) NSNKV_A3_INST(GG, true, 2) \
   NSNKV_A3_INST(GG, false, 0) NSNKV_A3_INST(GG, false, 1) NSNKV_A3_INST(GG, false, 2)

@@ -42,15 +42,15 @@ extern "C" size_t nsnkv_decode_workspace_bytes(const nsnkv_cache_view *cv_in) {
 
 template <int G, bool FOLD, int PREC>
 static int launch_attend(const CacheViewDev &cv, const float *q, float *out, float *lse,
-                         float *recs, int64_t total, cudaStream_t st) {
+                         float *recs, int64_t total, cudaStream_t st, const AppendRows &add) {
   int grid = attend_grid();
   if (total < grid) grid = (int)(total > 0 ? total : 1);
-  return nsnkv_launch_attend3<G, FOLD, PREC>(cv, q, out, lse, recs, total, grid, st);
+  return nsnkv_launch_attend3<G, FOLD, PREC>(cv, q, out, lse, recs, total, grid, st, add);
 }
 
-extern "C" int nsnkv_decode_attend(const nsnkv_cache_view *cv_in, const float *q, float *out,
-                                   float *lse, void *workspace, size_t workspace_bytes,
-                                   void *stream) {
+static int decode_attend(const nsnkv_cache_view *cv_in, const float *q, float *out, float *lse,
+                         void *workspace, size_t workspace_bytes, void *stream,
+                         const AppendRows &add) {
   CacheViewDev cv;
   int rc = make_cache_view(cv_in, &cv);
   if (rc) return rc;
@@ -80,9 +80,9 @@ extern "C" int nsnkv_decode_attend(const nsnkv_cache_view *cv_in, const float *q
   const bool fold = cv.cb_k.bit_mode == 2;
   const int prec = cv.precision;
 #define NSNKV_ATT_P(GG, FF)                                                       \
-  return prec == 0 ? launch_attend<GG, FF, 0>(cv, q, out, lse, recs, total, st)  \
-       : prec == 1 ? launch_attend<GG, FF, 1>(cv, q, out, lse, recs, total, st)  \
-                   : launch_attend<GG, FF, 2>(cv, q, out, lse, recs, total, st)
+  return prec == 0 ? launch_attend<GG, FF, 0>(cv, q, out, lse, recs, total, st, add)  \
+       : prec == 1 ? launch_attend<GG, FF, 1>(cv, q, out, lse, recs, total, st, add)  \
+                   : launch_attend<GG, FF, 2>(cv, q, out, lse, recs, total, st, add)
 #define NSNKV_ATT(GG)         \
   if (fold) NSNKV_ATT_P(GG, true); \
   else NSNKV_ATT_P(GG, false)
@@ -94,4 +94,25 @@ extern "C" int nsnkv_decode_attend(const nsnkv_cache_view *cv_in, const float *q
   }
 #undef NSNKV_ATT_P
 #undef NSNKV_ATT
+}
+
+extern "C" int nsnkv_decode_attend(const nsnkv_cache_view *cv, const float *q, float *out,
+                                   float *lse, void *workspace, size_t workspace_bytes,
+                                   void *stream) {
+  return decode_attend(cv, q, out, lse, workspace, workspace_bytes, stream, AppendRows{});
+}
+
+extern "C" int nsnkv_decode_step(const nsnkv_cache_view *cv, const float *q, const void *new_k,
+                                 const void *new_v, int32_t new_bf16, int32_t n_new,
+                                 int32_t *n_res_out, float *out, float *lse, void *workspace,
+                                 size_t workspace_bytes, void *stream) {
+  if (n_new < 1 || n_new >= R || !new_k || !new_v || !n_res_out)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "decode_step: need 1..63 new rows and n_res_out");
+  AppendRows add;
+  add.k = new_k;
+  add.v = new_v;
+  add.bf16 = new_bf16 ? 1 : 0;
+  add.n = n_new;
+  add.n_res_out = n_res_out;
+  return decode_attend(cv, q, out, lse, workspace, workspace_bytes, stream, add);
 }

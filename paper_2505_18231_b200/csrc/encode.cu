@@ -142,21 +142,45 @@ __device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1,
       : "r"(a0), "r"(a1), "r"(b0));
 }
 
+// 4 consecutive elements of a fp32 or bf16 row buffer as fp32 (bf16 -> fp32
+// is exact)
+__device__ __forceinline__ float4 load_row4(const void *base, int64_t off, int bf16) {
+  if (bf16) {
+    const uint2 raw = *reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(base) + off);
+    return make_float4(bf16_to_f32((uint16_t)(raw.x & 0xffffu)), bf16_to_f32((uint16_t)(raw.x >> 16)),
+                       bf16_to_f32((uint16_t)(raw.y & 0xffffu)), bf16_to_f32((uint16_t)(raw.y >> 16)));
+  }
+  return *reinterpret_cast<const float4 *>(static_cast<const float *>(base) + off);
+}
+
+// Where one chunk's 64 stream rows come from (kvcache.py:179-186): stream row
+// i of the unit is res[i] for i < n_resid, else fresh row i - n_resid, the
+// fresh rows of the unit being fresh[r * fresh_stride] (fp32 or bf16).
+struct ChunkSrc {
+  const float *res;      // the unit's residual rows [64][128] (fp32)
+  int n_resid;
+  const void *fresh;     // the unit's first fresh row
+  int64_t fresh_stride;  // elements between consecutive fresh rows
+  int fresh_bf16;
+  int k;                 // chunk index within this flush (stream rows 64 k ..)
+  int64_t pos_base;      // absolute position of the chunk's first token
+  uint8_t *page;         // destination page
+  int32_t *cnt_out;      // NSNKV_NUM_COUNTERS event counts, or nullptr
+  // after the rows are gathered (so the old residual is no longer read):
+  // copy res_n fresh rows starting at fresh row res_from into res_dst
+  float *res_dst;
+  int res_from, res_n;
+};
+
 template <bool FOLD>
-__global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_kernel(
-    const float *__restrict__ residual, int n_resid, const void *__restrict__ fresh, int fresh_bf16,
-    int64_t n_fresh, int n_flush, int is_key, const int64_t *__restrict__ start_pos,
-    const float2 *__restrict__ rope_cs, int64_t rope_pos0, int64_t rope_n, CodebookDev cb,
-    int strategy, uint8_t *__restrict__ pool, const int32_t *__restrict__ page_ids,
-    int page_id_stride, int32_t *__restrict__ counters) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  EncodeSmem &s = *reinterpret_cast<EncodeSmem *>(smem_raw);
+__device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, int is_key,
+                                             const float2 *__restrict__ rope_cs, int64_t rope_pos0,
+                                             int64_t rope_n, const CodebookDev &cb, int strategy) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int u = blockIdx.x / n_flush;
-  const int k = blockIdx.x - u * n_flush;
   const PageLayout L = page_layout(FOLD ? 2 : 1);
   constexpr bool fold = FOLD;
   const int g = lane >> 2, lt = lane & 3;  // mma fragment coordinates
+  const int k = J.k;
 
   if (tid < NSNKV_NUM_COUNTERS) s.cnt[tid] = 0;
   for (int i = tid; i < NENT * 8; i += ENC_THREADS) s.ent[i] = cb.entries[i];
@@ -170,24 +194,21 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
     const int t = i / (D / 4), c4 = i - t * (D / 4);
     const int64_t srow = (int64_t)k * R + t;
     float4 v;
-    if (srow < n_resid) {
-      v = *reinterpret_cast<const float4 *>(residual + ((int64_t)u * R + srow) * D + 4 * c4);
+    if (srow < J.n_resid) {
+      v = *reinterpret_cast<const float4 *>(J.res + srow * D + 4 * c4);
     } else {
-      const int64_t fr = (int64_t)u * n_fresh + (srow - n_resid);
-      if (fresh_bf16) {
-        const uint2 raw =
-            *reinterpret_cast<const uint2 *>(static_cast<const uint16_t *>(fresh) + fr * D + 4 * c4);
-        v.x = bf16_to_f32((uint16_t)(raw.x & 0xffffu));
-        v.y = bf16_to_f32((uint16_t)(raw.x >> 16));
-        v.z = bf16_to_f32((uint16_t)(raw.y & 0xffffu));
-        v.w = bf16_to_f32((uint16_t)(raw.y >> 16));
-      } else {
-        v = *reinterpret_cast<const float4 *>(static_cast<const float *>(fresh) + fr * D + 4 * c4);
-      }
+      v = load_row4(J.fresh, (srow - J.n_resid) * J.fresh_stride + 4 * c4, J.fresh_bf16);
     }
     *reinterpret_cast<float4 *>(&s.x[t][4 * c4]) = v;
   }
   __syncthreads();
+  if (J.res_dst) {  // the unit's new residual rows (its old ones are in s.x now)
+    for (int i = tid; i < J.res_n * (D / 4); i += ENC_THREADS) {
+      const int t = i / (D / 4), c4 = i - t * (D / 4);
+      *reinterpret_cast<float4 *>(J.res_dst + (int64_t)t * D + 4 * c4) =
+          load_row4(J.fresh, (int64_t)(J.res_from + t) * J.fresh_stride + 4 * c4, J.fresh_bf16);
+    }
+  }
 
   // ---- 2. nsn_forward (nsn.py:68-85) --------------------------------------
   int clamps = scale_rows(s, s.s1);
@@ -208,7 +229,7 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
 
   // ---- 3. keys: RoPE at absolute positions, then FWHT (kvcache.py:121-123)
   if (is_key) {
-    const int64_t pos_base = start_pos[u] + (int64_t)k * R;
+    const int64_t pos_base = J.pos_base;
     for (int t = warp; t < R; t += ENC_THREADS / 32) {
       int64_t row = pos_base + t - rope_pos0;
       row = row < 0 ? 0 : (row >= rope_n ? rope_n - 1 : row);
@@ -466,7 +487,7 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
   __syncthreads();
 
   // ---- 6. pack the page ----------------------------------------------------
-  uint8_t *page = pool + (int64_t)page_ids[(int64_t)u * page_id_stride + k] * L.bytes;
+  uint8_t *page = J.page;
   // indices: 1024 bytes, 4 per thread
   {
     const uint32_t w = *reinterpret_cast<const uint32_t *>(&s.idx[0][0] + 4 * tid);
@@ -551,8 +572,36 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_ker
     // zero the page padding so pages are deterministic byte images
     for (int i = L.ledger + lane; i < L.bytes; i += 32) page[i] = 0;
   }
-  if (counters && tid < NSNKV_NUM_COUNTERS)
-    counters[(int64_t)blockIdx.x * NSNKV_NUM_COUNTERS + tid] = s.cnt[tid];
+  if (J.cnt_out && tid < NSNKV_NUM_COUNTERS) J.cnt_out[tid] = s.cnt[tid];
+}
+
+// nsnkv_encode_chunks: chunk k of unit u per CTA, every unit flushing n_flush
+template <bool FOLD>
+__global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS) encode_chunks_kernel(
+    const float *__restrict__ residual, int n_resid, const void *__restrict__ fresh, int fresh_bf16,
+    int64_t n_fresh, int n_flush, int is_key, const int64_t *__restrict__ start_pos,
+    const float2 *__restrict__ rope_cs, int64_t rope_pos0, int64_t rope_n, CodebookDev cb,
+    int strategy, uint8_t *__restrict__ pool, const int32_t *__restrict__ page_ids,
+    int page_id_stride, int32_t *__restrict__ counters) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EncodeSmem &s = *reinterpret_cast<EncodeSmem *>(smem_raw);
+  const int u = blockIdx.x / n_flush;
+  const int k = blockIdx.x - u * n_flush;
+  const PageLayout L = page_layout(FOLD ? 2 : 1);
+  ChunkSrc J;
+  J.res = residual + (int64_t)u * R * D;
+  J.n_resid = n_resid;
+  J.fresh_bf16 = fresh_bf16;
+  J.fresh = fresh_bf16 ? (const void *)(static_cast<const uint16_t *>(fresh) + (int64_t)u * n_fresh * D)
+                       : (const void *)(static_cast<const float *>(fresh) + (int64_t)u * n_fresh * D);
+  J.fresh_stride = D;
+  J.k = k;
+  J.pos_base = is_key ? start_pos[u] + (int64_t)k * R : 0;
+  J.page = pool + (int64_t)page_ids[(int64_t)u * page_id_stride + k] * L.bytes;
+  J.cnt_out = counters ? counters + (int64_t)blockIdx.x * NSNKV_NUM_COUNTERS : nullptr;
+  J.res_dst = nullptr;
+  J.res_from = J.res_n = 0;
+  encode_chunk<FOLD>(s, J, is_key, rope_cs, rope_pos0, rope_n, cb, strategy);
 }
 
 }  // namespace nsnkv
@@ -592,4 +641,96 @@ extern "C" int nsnkv_encode_chunks(const float *residual, int32_t n_resid, const
       page_id_stride, counters);
   nsnkv_internal_count_launch(1);
   return nsnkv_internal_check_launch("encode_chunks");
+}
+
+// ---------------------------------------------------------------------------
+// nsnkv_append: one launch per append of any shape (uniform or per-unit
+// token counts): every full chunk of every unit is flushed into the page the
+// caller allocated for it, the new residual rows are written, and the page
+// table and per-unit counters are updated on the device (kvcache.py:157-195).
+// grid = (n_units * max(max_flush, 1), 2 kinds); CTA (u, k, kind):
+//   k < n_flush[u]          encode chunk k of the unit's stream into
+//                           new_pages[u][k]; k == 0 also writes the new
+//                           residual rows (after gathering the old ones)
+//   k == 0, n_flush[u] == 0 append the fresh rows to the residual
+// Counters are double-buffered (in -> out) so no CTA reads a value another
+// CTA of the same launch writes; the kind-0 CTA with k == 0 owns them.
+// ---------------------------------------------------------------------------
+template <bool FOLD>
+__global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS)
+    append_kernel(nsnkv_append_args a, CodebookDev cbk, CodebookDev cbv) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EncodeSmem &s = *reinterpret_cast<EncodeSmem *>(smem_raw);
+  const int fmax = a.max_flush > 0 ? a.max_flush : 1;
+  const int u = blockIdx.x / fmax, k = blockIdx.x - u * fmax;
+  const int kind = blockIdx.y;  // 0 keys, 1 values
+  const int n_res = a.n_res_in[u], n_ch = a.n_chunks_in[u];
+  const int64_t n_new = a.new_count ? (int64_t)a.new_count[u] : a.n_new_uniform;
+  const int64_t off = a.fresh_off ? a.fresh_off[u] : (int64_t)u * a.n_new_uniform;
+  const int n_flush = (int)((n_res + n_new) / R);
+  const int64_t stride = a.fresh_row_stride * D;  // elements between a unit's fresh rows
+  const void *fresh = kind ? a.fresh_v : a.fresh_k;
+  const void *fresh_u = a.fresh_bf16 ? (const void *)(static_cast<const uint16_t *>(fresh) + off * D)
+                                     : (const void *)(static_cast<const float *>(fresh) + off * D);
+  float *res = (kind ? a.v_res : a.k_res) + (int64_t)u * R * D;
+  const int new_res = (int)(n_res + n_new - (int64_t)n_flush * R);
+  if (k < n_flush) {
+    const PageLayout L = page_layout(FOLD ? 2 : 1);
+    const int32_t pid = a.new_pages[(int64_t)u * a.max_flush + k];
+    ChunkSrc J;
+    J.res = res;
+    J.n_resid = n_res;
+    J.fresh = fresh_u;
+    J.fresh_stride = stride;
+    J.fresh_bf16 = a.fresh_bf16;
+    J.k = k;
+    J.pos_base = a.base_pos[u] + (int64_t)(n_ch + k) * R;
+    J.page = (kind ? a.v_pool : a.k_pool) + (int64_t)pid * L.bytes;
+    J.cnt_out = a.counters ? a.counters + ((int64_t)pid * 2 + kind) * NSNKV_NUM_COUNTERS : nullptr;
+    J.res_dst = k == 0 ? res : nullptr;
+    J.res_from = (int)((int64_t)n_flush * R - n_res);
+    J.res_n = new_res;
+    encode_chunk<FOLD>(s, J, kind == 0, reinterpret_cast<const float2 *>(a.rope_cs), a.rope_pos0,
+                       a.rope_n, kind ? cbv : cbk, a.strategy);
+    if (kind == 0 && threadIdx.x == 0) a.page_table[(int64_t)u * a.page_table_stride + n_ch + k] = pid;
+  } else if (k == 0) {  // no flush: the fresh rows join the residual
+    for (int i = threadIdx.x; i < (int)n_new * (D / 4); i += ENC_THREADS) {
+      const int t = i / (D / 4), c4 = i - t * (D / 4);
+      *reinterpret_cast<float4 *>(res + (int64_t)(n_res + t) * D + 4 * c4) =
+          load_row4(fresh_u, (int64_t)t * stride + 4 * c4, a.fresh_bf16);
+    }
+  }
+  if (kind == 0 && k == 0 && threadIdx.x == 0) {
+    a.n_chunks_out[u] = n_ch + n_flush;
+    a.n_res_out[u] = new_res;
+  }
+}
+
+extern "C" int nsnkv_append(const nsnkv_append_args *a, void *stream) {
+  if (!a || a->n_units < 0 || a->max_flush < 0 || a->fresh_row_stride < 1)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "append: bad sizes");
+  if (!a->n_res_in || !a->n_chunks_in || !a->n_res_out || !a->n_chunks_out || !a->k_res ||
+      !a->v_res || !a->base_pos || (a->max_flush > 0 && (!a->new_pages || !a->page_table)))
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "append: null cache buffers");
+  if (a->strategy < 0 || a->strategy > 3)
+    return nsnkv_internal_set_error(NSNKV_ERR_UNSUPPORTED, "append: unknown strategy");
+  if (a->max_flush > 0 && (!a->rope_cs || a->rope_n <= 0))
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "append: keys need a RoPE table");
+  if (a->n_units == 0) return NSNKV_OK;
+  CodebookDev ck, cv;
+  int rc = nsnkv_internal_codebook_dev(a->cb_k, &ck);
+  if (!rc) rc = nsnkv_internal_codebook_dev(a->cb_v, &cv);
+  if (rc) return rc;
+  if (ck.bit_mode != cv.bit_mode)
+    return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "append: codebook bit modes differ");
+  const size_t smem = sizeof(EncodeSmem);
+  static unsigned long long attr_k = 0, attr_v = 0;
+  set_smem_attr_once(append_kernel<true>, (int)smem, attr_k, 100);
+  set_smem_attr_once(append_kernel<false>, (int)smem, attr_v, 100);
+  const int fmax = a->max_flush > 0 ? a->max_flush : 1;
+  const dim3 grid((unsigned)((int64_t)a->n_units * fmax), 2);
+  auto kern = ck.bit_mode == 2 ? append_kernel<true> : append_kernel<false>;
+  kern<<<grid, ENC_THREADS, smem, (cudaStream_t)stream>>>(*a, ck, cv);
+  nsnkv_internal_count_launch(1);
+  return nsnkv_internal_check_launch("append");
 }

@@ -55,12 +55,12 @@ def test_reserve_presizes_and_keeps_results():
     k = torch.randn(B, H, T, 128, device="cuda", generator=g)
     v = torch.randn(B, H, T, 128, device="cuda", generator=g)
     a = _cache("2b", B, H).reserve(T)
-    pools = (a.k_pool.data_ptr(), a.v_pool.data_ptr(), a.max_chunks)
+    pools = (a.pool_ptrs(), a.capacity, a.max_chunks)
     b = _cache("2b", B, H)
     for i in range(0, T, 7):
         a.append(k[:, :, i:i + 7], v[:, :, i:i + 7])
         b.append(k[:, :, i:i + 7], v[:, :, i:i + 7])
-    assert (a.k_pool.data_ptr(), a.v_pool.data_ptr(), a.max_chunks) == pools
+    assert (a.pool_ptrs(), a.capacity, a.max_chunks) == pools
     for u in range(B * H):
         assert a.snapshot(u) == b.snapshot(u)
     q = torch.randn(B, 4 * H, 128, device="cuda", generator=g)

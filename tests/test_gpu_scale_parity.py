@@ -39,11 +39,9 @@ def _misaligned_torch(shape, gen):
 
 
 def _wire_all(cache, kind):
-    pool = cache.k_pool if kind == "k" else cache.v_pool
-    ids = cache.page_table[:, :cache.n_chunks].reshape(-1).long()
     from paper_2505_18231_b200.cache import pages_to_wire
 
-    return pages_to_wire(pool[ids].cpu().numpy(), cache.bit_mode, cache.config.strategy, kind)
+    return pages_to_wire(cache.all_pages(kind), cache.bit_mode, cache.config.strategy, kind)
 
 
 @pytest.mark.parametrize("mode,dist", [("2b", "normal"), ("1b", "mis")])

@@ -159,7 +159,7 @@ def test_status_codes_map_to_reference_exceptions():
 
 def _header_symbols() -> set[str]:
     text = (ROOT / "include" / "nsnkv_b200.h").read_text()
-    return set(re.findall(r"^\s*(?:int|size_t|int64_t|const char \*)\s*(nsnkv_\w+)\(", text, re.M))
+    return set(re.findall(r"^\s*(?:int|size_t|int64_t|const char \*|void \*)\s*(nsnkv_\w+)\(", text, re.M))
 
 
 def test_c_abi_library_exports_every_header_symbol():
