@@ -410,10 +410,26 @@ def run_ours(args) -> dict | None:
                 extras[name] = measure_config(name, device, peak, steps=max(10, args.steps // 5))
         res["extras"] = extras
         res["encode"] = {f"{m}b": measure_encode(device, m) for m in (2, 1)}
+        if args.config == "c2" and not args.no_model:
+            res["c5_model"] = measure_c5(device)
         res["parity"] = c1_parity()
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
     return res
+
+
+def measure_c5(device) -> dict:
+    """BASELINE config 5 per GPU: full LLaMA-3.1-8B-shape random-init decode
+    step, batch 32 x 16K (the per-GPU share of batch 256 on 8 GPUs, DP=8),
+    NSNQuant 1-bit KV (fused decode_step) vs bf16 KV (flash-attn)."""
+    sys.path.insert(0, str(ROOT / "scripts"))
+    import bench_model as BM
+
+    out = {}
+    for kv in ("nsn1b", "bf16"):
+        out[kv] = BM.run(kv, 32, 16384, 32, steps=6, warmup=2, dev=device)
+    out["speedup_vs_bf16"] = round(out["nsn1b"]["tokens_per_s_job"] / out["bf16"]["tokens_per_s_job"], 3)
+    return out
 
 
 def kernel_line(sbytes: int, ms: float, peak: float) -> dict:
@@ -634,6 +650,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the serving-step and encode measurements")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-model", action="store_true", help="skip the C5 full-model extra")
     ap.add_argument("--precision", default=None, choices=["precise", "vfast"],
                     help="decode codeword precision (DESIGN.md 3.2); default: the library's "
                          "(vfast for 2-bit, precise for 1-bit)")

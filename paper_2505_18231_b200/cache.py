@@ -408,13 +408,12 @@ class PagedKvCache:
         if fmax:
             self._ensure_width(int((self.unit_n_chunks + n_flush).max()))
             ids = self._alloc(int(n_flush.sum()))
+            # unit-major: unit u takes the next n_flush[u] ids
+            mask = np.arange(fmax)[None, :] < n_flush[:, None]
             npg = np.zeros((U, fmax), np.int32)
-            pos = 0
-            for u in np.nonzero(n_flush)[0]:
-                f = int(n_flush[u])
-                npg[u, :f] = ids[pos:pos + f]
-                self._pt[u, self.unit_n_chunks[u]:self.unit_n_chunks[u] + f] = ids[pos:pos + f]
-                pos += f
+            npg[mask] = ids
+            rows, ks = np.nonzero(mask)
+            self._pt[rows, self.unit_n_chunks[rows] + ks] = ids
             new_pages_t = self._upload(npg)
         table = self.rope.ensure(int((self.unit_base + (self.unit_n_chunks + n_flush) * R).max()) + R)
         a = _lib.AppendArgs()

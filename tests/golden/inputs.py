@@ -139,3 +139,24 @@ def c1_inputs():
         yield {"name": name, "bit_mode": bm, "distinct_v": distinct,
                "batches": [(0, 3001), (3001, C1_TOKENS)],
                "keys": K, "values_ht": V, "q": q}
+
+
+def kernels_parity_inputs():
+    """The inputs of reference pkg/tests/test_kernels_parity.py:14-57, drawn
+    in that file's order (make_rng = PCG64(seed); sample_standard_normal =
+    rng.standard_normal((rows, cols), float32))."""
+    fwht = {d: rng(d).standard_normal((33, d), dtype=np.float32) for d in (2, 8, 64, 128, 1024)}
+    match = {}
+    for fold in (True, False):
+        g = rng(99)
+        entries = np.abs(g.standard_normal((256, 8), dtype=np.float32)) + np.float32(0.01)
+        if not fold:
+            entries = g.standard_normal((256, 8), dtype=np.float32) + np.float32(0.01)
+        vecs = g.standard_normal((50000, 8), dtype=np.float32)
+        match["fold" if fold else "nofold"] = (vecs, entries, fold)
+    g = rng(5)
+    entries = g.standard_normal((256, 8), dtype=np.float32)
+    entries[128:] = entries[:128]  # every entry duplicated
+    vecs = g.standard_normal((5000, 8), dtype=np.float32)
+    match["near_ties"] = (vecs, entries, False)
+    return {"fwht": fwht, "match": match}
