@@ -648,7 +648,7 @@ extern "C" int nsnkv_encode_chunks(const float *residual, int32_t n_resid, const
 // token counts): every full chunk of every unit is flushed into the page the
 // caller allocated for it, the new residual rows are written, and the page
 // table and per-unit counters are updated on the device (kvcache.py:157-195).
-// grid = (n_units * max(max_flush, 1), 2 kinds); CTA (u, k, kind):
+// two launches (keys, then values), grid n_units * max(max_flush, 1); CTA (u, k):
 //   k < n_flush[u]          encode chunk k of the unit's stream into
 //                           new_pages[u][k]; k == 0 also writes the new
 //                           residual rows (after gathering the old ones)
@@ -656,14 +656,14 @@ extern "C" int nsnkv_encode_chunks(const float *residual, int32_t n_resid, const
 // Counters are double-buffered (in -> out) so no CTA reads a value another
 // CTA of the same launch writes; the kind-0 CTA with k == 0 owns them.
 // ---------------------------------------------------------------------------
-template <bool FOLD>
+template <bool FOLD, int KIND>
 __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS)
-    append_kernel(nsnkv_append_args a, CodebookDev cbk, CodebookDev cbv) {
+    append_kernel(nsnkv_append_args a, CodebookDev cb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EncodeSmem &s = *reinterpret_cast<EncodeSmem *>(smem_raw);
   const int fmax = a.max_flush > 0 ? a.max_flush : 1;
   const int u = blockIdx.x / fmax, k = blockIdx.x - u * fmax;
-  const int kind = blockIdx.y;  // 0 keys, 1 values
+  constexpr int kind = KIND;  // 0 keys, 1 values
   const int n_res = a.n_res_in[u], n_ch = a.n_chunks_in[u];
   const int64_t n_new = a.new_count ? (int64_t)a.new_count[u] : a.n_new_uniform;
   const int64_t off = a.fresh_off ? a.fresh_off[u] : (int64_t)u * a.n_new_uniform;
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(ENC_THREADS, ENC_MIN_BLOCKS)
     J.res_from = (int)((int64_t)n_flush * R - n_res);
     J.res_n = new_res;
     encode_chunk<FOLD>(s, J, kind == 0, reinterpret_cast<const float2 *>(a.rope_cs), a.rope_pos0,
-                       a.rope_n, kind ? cbv : cbk, a.strategy);
+                       a.rope_n, cb, a.strategy);
     if (kind == 0 && threadIdx.x == 0) a.page_table[(int64_t)u * a.page_table_stride + n_ch + k] = pid;
   } else if (k == 0) {  // no flush: the fresh rows join the residual
     for (int i = threadIdx.x; i < (int)n_new * (D / 4); i += ENC_THREADS) {
@@ -724,13 +724,23 @@ extern "C" int nsnkv_append(const nsnkv_append_args *a, void *stream) {
   if (ck.bit_mode != cv.bit_mode)
     return nsnkv_internal_set_error(NSNKV_ERR_SHAPE, "append: codebook bit modes differ");
   const size_t smem = sizeof(EncodeSmem);
-  static unsigned long long attr_k = 0, attr_v = 0;
-  set_smem_attr_once(append_kernel<true>, (int)smem, attr_k, 100);
-  set_smem_attr_once(append_kernel<false>, (int)smem, attr_v, 100);
+  static unsigned long long attr[4] = {0, 0, 0, 0};
+  set_smem_attr_once(append_kernel<true, 0>, (int)smem, attr[0], 100);
+  set_smem_attr_once(append_kernel<true, 1>, (int)smem, attr[1], 100);
+  set_smem_attr_once(append_kernel<false, 0>, (int)smem, attr[2], 100);
+  set_smem_attr_once(append_kernel<false, 1>, (int)smem, attr[3], 100);
   const int fmax = a->max_flush > 0 ? a->max_flush : 1;
-  const dim3 grid((unsigned)((int64_t)a->n_units * fmax), 2);
-  auto kern = ck.bit_mode == 2 ? append_kernel<true> : append_kernel<false>;
-  kern<<<grid, ENC_THREADS, smem, (cudaStream_t)stream>>>(*a, ck, cv);
-  nsnkv_internal_count_launch(1);
+  const unsigned grid = (unsigned)((int64_t)a->n_units * fmax);
+  cudaStream_t st = (cudaStream_t)stream;
+  // values first: the key launch owns the counters (double-buffered, so the
+  // order does not matter for correctness)
+  if (ck.bit_mode == 2) {
+    append_kernel<true, 1><<<grid, ENC_THREADS, smem, st>>>(*a, cv);
+    append_kernel<true, 0><<<grid, ENC_THREADS, smem, st>>>(*a, ck);
+  } else {
+    append_kernel<false, 1><<<grid, ENC_THREADS, smem, st>>>(*a, cv);
+    append_kernel<false, 0><<<grid, ENC_THREADS, smem, st>>>(*a, ck);
+  }
+  nsnkv_internal_count_launch(2);
   return nsnkv_internal_check_launch("append");
 }

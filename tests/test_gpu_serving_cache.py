@@ -144,9 +144,10 @@ def test_growth_never_moves_pages():
         assert np.array_equal(c.pages(u, "k")[:3], first[u])
 
 
-def test_decode_step_is_one_launch_without_host_sync():
-    """A decode step's append (1 token per sequence) is a single kernel
-    launch; a server loop of append + attend never reads device memory."""
+def test_decode_step_launches_and_no_host_sync():
+    """A serving decode step (1 token per sequence) adds no launch to the
+    attention's two unless a chunk completes (then nsnkv_append's two);
+    the loop never reads device memory (the host mirrors every length)."""
     from paper_2505_18231_b200 import _lib
 
     c = _cache(2, 4, 8, check_finite=False).reserve(64 * 3)
@@ -158,9 +159,8 @@ def test_decode_step_is_one_launch_without_host_sync():
     torch.cuda.synchronize()
     n0 = _lib.launch_count()
     for i in range(8):  # crosses a chunk boundary (60 + 8 > 64)
-        c.append(tok[i], tok[i])
-        c.attend(q, out=out)
-    assert _lib.launch_count() - n0 == 8 * 3  # append + attend + combine
+        c.decode_step(q, tok[i], tok[i], out=out)
+    assert _lib.launch_count() - n0 == 8 * 2 + 2  # attend + combine each step, one flush (2 launches)
     assert c.unit_n_chunks.tolist() == [3] * 32 and c.unit_n_res.tolist() == [4] * 32
 
 
