@@ -18,6 +18,8 @@
  *   nsnkv_codebook_create  -> codebook.py:71-106 (Codebook, inv_norms) and
  *                             kernels/__init__.py:44-51 (entry_inv_norms)
  *   nsnkv_rope_table       -> rope.py:29-51 (_pair_freqs, rope_rows angles)
+ *   nsnkv_kmeans_assign,
+ *   nsnkv_finetune_stats   -> codebook.py:175-340 (kmeans_init, finetune)
  *   nsnkv_encode_chunks    -> kvcache.py:114-154 (flush_chunk_keys/values):
  *                             nsn.py:68-85, rope.py:35-51, hadamard.py:65-83,
  *                             vq.py:211-279 in one kernel
@@ -119,6 +121,23 @@ int nsnkv_codebook_create(const float *entries_host, const double *inv_norms_hos
                           int32_t bit_mode, nsnkv_codebook **out);
 int nsnkv_codebook_destroy(nsnkv_codebook *cb);
 int nsnkv_codebook_bit_mode(const nsnkv_codebook *cb);
+
+/* ---- codebook build passes (codebook.py:175-340) ---------------------- */
+/* One Lloyd iteration of kmeans_init (codebook.py:196-212) over data[n][8]
+ * (fp32) against centroids[256][8] (fp64): assign[i] = argmax_c of
+ * x.f32(c) - 0.5 f32(|c|^2) (first maximum); sums[256][8] (fp64) and
+ * counts[256] (caller-zeroed) accumulate the assigned points; d2[i] (may be
+ * NULL) = |x|^2 - 2 x.c + |c|^2 for the empty-cluster reseed. */
+int nsnkv_kmeans_assign(const float *data, int64_t n, const double *centroids, int32_t *assign,
+                        double *sums, int32_t *counts, double *d2, void *stream);
+/* Statistics of one finetune step (codebook.py:300-318) for batch[n][8]
+ * assigned to idx[n] (the nsnkv_match_block rule): per-entry sums of the
+ * samples' unit vectors and of their cosines to entries[256][8] (fp64),
+ * counts of live (non-zero) samples, and += the batch's summed cosine
+ * distance.  Accumulators are caller-zeroed. */
+int nsnkv_finetune_stats(const float *batch, int64_t n, const int32_t *idx,
+                         const double *entries, double *sum_unit, double *sum_cos,
+                         int32_t *counts, double *cosdist, void *stream);
 
 /* ---- RoPE table (rope.py:29-51) --------------------------------------- */
 /* out[n][64][2] = float32(cos/sin(float64(pos0 + i) * freqs[j])) for

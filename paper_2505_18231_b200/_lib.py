@@ -122,6 +122,10 @@ _SIGS = {
                              c_size, c_void_p], c_int),
     "nsnkv_decode_workspace_bytes": ([ctypes.POINTER(CacheView)], c_size),
     "nsnkv_append": ([ctypes.POINTER(AppendArgs), c_void_p], c_int),
+    "nsnkv_kmeans_assign": ([c_void_p, c_i64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                             c_void_p], c_int),
+    "nsnkv_finetune_stats": ([c_void_p, c_i64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                              c_void_p, c_void_p], c_int),
     "nsnkv_decode_step": ([ctypes.POINTER(CacheView), c_void_p, c_void_p, c_void_p, c_int, c_int,
                            c_void_p, c_void_p, c_void_p, c_void_p, c_size, c_void_p], c_int),
     "nsnkv_pool_create": ([c_size, ctypes.POINTER(c_void_p)], c_int),

@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libnsnkv_b200.so"
 
-SOURCES = ["capi.cu", "pool.cu", "level1.cu", "encode.cu", "decode_ref.cu", "decode_dispatch.cu", "decode_attend3.cu"]
+SOURCES = ["capi.cu", "pool.cu", "level1.cu", "encode.cu", "decode_ref.cu", "decode_dispatch.cu", "decode_attend3.cu", "codebook_build.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
