@@ -52,7 +52,6 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
   if (bit_mode != 1 && bit_mode != 2)
     return nsnkv_internal_set_error(NSNKV_ERR_FORMAT, "codebook: bit_mode must be 1 or 2");
   std::vector<double> inv(NENT);
-  std::vector<float> inv32(NENT);
   for (int c = 0; c < NENT; ++c) {
     const float *e = entries_host + 8 * c;
     if (bit_mode == 2)
@@ -68,7 +67,6 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
       if (s < 1e-24) return nsnkv_internal_set_error(NSNKV_ERR_FORMAT, "codebook contains a zero entry");
       inv[c] = 1.0 / std::sqrt(s);
     }
-    inv32[c] = (float)inv[c];
   }
   // decode gather table: row c = [hi codeword x 8 slots][lo codeword x 8 slots]
   std::vector<uint4> tw(NENT * 16);
@@ -86,29 +84,33 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
       tw[c * 16 + 8 + slot] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
   }
-  // encode search B fragments: normalized entries split into fp16 hi + lo
-  std::vector<uint2> mb(32 * 32);
-  for (int nt = 0; nt < 32; ++nt)
-    for (int L = 0; L < 32; ++L) {
-      const int c = 8 * nt + (L >> 2), t = L & 3;
-      const float *e = entries_host + 8 * c;
-      const float a = (float)((double)e[2 * t] * inv[c]), b = (float)((double)e[2 * t + 1] * inv[c]);
-      const float ah = __half2float(__float2half_rn(a)), bh = __half2float(__float2half_rn(b));
-      mb[nt * 32 + L] = make_uint2(pack_half2(a, b), pack_half2(a - ah, b - bh));
+  // encode search B operands (tcgen05, K-major no-swizzle canonical layout):
+  // matrix m (0: [e_hi | e_hi], 1: [e_lo | e_lo]) of the normalized entries
+  std::vector<uint16_t> tb(2 * NENT * 16);
+  for (int c = 0; c < NENT; ++c) {
+    const float *e = entries_host + 8 * c;
+    for (int k = 0; k < 8; ++k) {
+      const float a = (float)((double)e[k] * inv[c]);
+      const __half h = __float2half_rn(a);
+      const __half l = __float2half_rn(a - __half2float(h));
+      for (int kh = 0; kh < 2; ++kh) {
+        const size_t off = (size_t)(c / 8) * 128 + kh * 64 + (c % 8) * 8 + k;  // in halves
+        tb[off] = __half_as_ushort(h);
+        tb[NENT * 16 + off] = __half_as_ushort(l);
+      }
     }
+  }
   nsnkv_codebook *cb = new nsnkv_codebook();
   cb->dev.bit_mode = bit_mode;
   cudaError_t err = cudaSuccess;
   err = cudaMalloc(&cb->dev.entries, NENT * 8 * sizeof(float));
   if (!err) err = cudaMalloc(&cb->dev.inv, NENT * sizeof(double));
-  if (!err) err = cudaMalloc(&cb->dev.inv32, NENT * sizeof(float));
   if (!err) err = cudaMalloc(&cb->dev.tabw, NENT * 16 * sizeof(uint4));
-  if (!err) err = cudaMalloc(&cb->dev.mma_b, 32 * 32 * sizeof(uint2));
+  if (!err) err = cudaMalloc(&cb->dev.tcb, 2 * NENT * 16 * sizeof(uint16_t));
   if (!err) err = cudaMemcpy(cb->dev.entries, entries_host, NENT * 8 * sizeof(float), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(cb->dev.inv, inv.data(), NENT * sizeof(double), cudaMemcpyHostToDevice);
-  if (!err) err = cudaMemcpy(cb->dev.inv32, inv32.data(), NENT * sizeof(float), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(cb->dev.tabw, tw.data(), NENT * 16 * sizeof(uint4), cudaMemcpyHostToDevice);
-  if (!err) err = cudaMemcpy(cb->dev.mma_b, mb.data(), 32 * 32 * sizeof(uint2), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(cb->dev.tcb, tb.data(), 2 * NENT * 16 * sizeof(uint16_t), cudaMemcpyHostToDevice);
   if (err) {
     nsnkv_codebook_destroy(cb);
     snprintf(g_err, sizeof(g_err), "codebook upload: %s", cudaGetErrorString(err));
@@ -122,9 +124,8 @@ extern "C" int nsnkv_codebook_destroy(nsnkv_codebook *cb) {
   if (!cb) return NSNKV_OK;
   cudaFree(cb->dev.entries);
   cudaFree(cb->dev.inv);
-  cudaFree(cb->dev.inv32);
   cudaFree(cb->dev.tabw);
-  cudaFree(cb->dev.mma_b);
+  cudaFree(cb->dev.tcb);
   delete cb;
   return NSNKV_OK;
 }

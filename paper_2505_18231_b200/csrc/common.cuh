@@ -48,16 +48,17 @@ __host__ __device__ constexpr PageLayout page_layout(int bit_mode) {
 struct CodebookDev {
   float *entries;      // [256][8] fp32 (codebook.py active_entries)
   double *inv;         // [256] fp64 1/||e|| (kernels/__init__.py:44-51)
-  float *inv32;        // [256] fp32 copy for the pre-pass
   // decode gather table (64 KB): row c = 256 bytes = [hi x 8 slots][lo x 8
   // slots], each slot the whole codeword as 8 fp16 (hi = fp16(e),
   // lo = fp16(e - hi)); 8 replicas so a quarter-warp of 16-byte loads with
   // slot = lane % 8 never bank-conflicts.
   uint4 *tabw;
-  // encode search B fragments (mma.sync m16n8k16): [n-tile 32][lane 32] of
-  // (fp16 hi, fp16 lo) halves of the normalized entry e_c / ||e_c|| at
-  // components 2t, 2t+1 of entry c = 8 n-tile + lane / 4.
-  uint2 *mma_b;
+  // encode search B operands for tcgen05.mma (16 KB, the shared-memory
+  // image): normalized entries e_c / ||e_c|| split into fp16 hi + lo, two
+  // K = 16 matrices [e_hi | e_hi] and [e_lo | e_lo] (row c), each in the
+  // no-swizzle K-major canonical layout: byte (c / 8) * 256 + khalf * 128 +
+  // (c % 8) * 16.
+  uint4 *tcb;
   int bit_mode;
 };
 

@@ -14,30 +14,43 @@
 #include "common.cuh"
 #include "decode_att.cuh"
 #include "match.cuh"
+#include "tc05.cuh"
 
 namespace nsnkv {
 
 constexpr int ENC_THREADS = 256;
+// TMEM columns per CTA for the codebook search: one round of the search
+// scores 128 sub-vectors against ENC_NCOL entries (tcgen05.mma M = 128,
+// N = ENC_NCOL), so 256 / ENC_NCOL rounds cover the codebook; at most
+// 512 / ENC_NCOL CTAs share an SM's tensor memory.
+#ifndef ENC_NCOL
+#define ENC_NCOL 128
+#endif
 // resident CTAs per SM the register budget is sized for: the phases of a
 // chunk are separated by block barriers, so more CTAs keep the SM busy while
-// others wait (4 CTAs: 64 registers, a few bytes of spill; 3.5 % faster than 3)
+// others wait (bounded by shared memory and the TMEM budget above)
 #ifndef ENC_MIN_BLOCKS
-#define ENC_MIN_BLOCKS 4
+#define ENC_MIN_BLOCKS 3
 #endif
+static_assert(ENC_MIN_BLOCKS * ENC_NCOL <= 512, "TMEM oversubscribed");
 constexpr int XS = D + 4;  // padded smem row stride (floats)
 
 struct EncodeSmem {
   float x[R][XS];                 // working rows
+  __align__(128) uint16_t tcb[2 * NENT * 16];  // search B operands (CodebookDev::tcb image)
+  __align__(128) uint16_t atile[2][128 * 16];  // search A operands (double-buffered): 128 sub-vectors [u_hi | u_lo]
   __align__(16) float ent[NENT * 8];
   double inv[NENT];
-  float inv32[NENT];
+  float2 rec[2][128];             // per column half: best score, index | near-tie flag
   float s1[R], s2[R], o[D];
-  uint2 mb[32][32];               // search B fragments (normalized entries hi/lo)
   uint16_t zmask[R];              // zero sub-vectors per token (bit j)
   float s2adj[R];
   uint8_t idx[R][NSUB];
   uint8_t sgn[R][NSUB];
   int cnt[NSNKV_NUM_COUNTERS];
+  uint64_t mbar;                  // tcgen05.commit -> search rounds
+  uint64_t tbar;                  // bulk copies of the codebook tables
+  uint32_t tmem_base;
 };
 
 // fp64 sum of squares of one token row held 4-per-lane (lane l owns
@@ -133,15 +146,6 @@ __device__ __forceinline__ uint32_t rtn4_level(float v, float zero32f, float sca
   return (uint32_t)lv;
 }
 
-// D += A (16 x 8, fp16, row) . B (8 x 8, fp16, col), fp32 accumulate
-__device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(b0));
-}
-
 // 4 consecutive elements of a fp32 or bf16 row buffer as fp32 (bf16 -> fp32
 // is exact)
 __device__ __forceinline__ float4 load_row4(const void *base, int64_t off, int bf16) {
@@ -179,16 +183,24 @@ __device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, i
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const PageLayout L = page_layout(FOLD ? 2 : 1);
   constexpr bool fold = FOLD;
-  const int g = lane >> 2, lt = lane & 3;  // mma fragment coordinates
   const int k = J.k;
 
   if (tid < NSNKV_NUM_COUNTERS) s.cnt[tid] = 0;
-  for (int i = tid; i < NENT * 8; i += ENC_THREADS) s.ent[i] = cb.entries[i];
-  for (int i = tid; i < NENT; i += ENC_THREADS) {
-    s.inv[i] = cb.inv[i];
-    s.inv32[i] = cb.inv32[i];
+  // codebook tables by bulk copy (TMA engine), overlapping the row gather;
+  // TMEM for the search scores
+  if (warp == 0) {
+    tc05::alloc(smem_u32(&s.tmem_base), ENC_NCOL);
+    tc05::relinquish();
+    if (lane == 0) {
+      mbar_init(&s.mbar, 1);
+      mbar_init(&s.tbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&s.tbar, (uint32_t)(sizeof(s.tcb) + sizeof(s.ent) + sizeof(s.inv)));
+      tma_load_1d(s.tcb, cb.tcb, sizeof(s.tcb), &s.tbar);
+      tma_load_1d(s.ent, cb.entries, sizeof(s.ent), &s.tbar);
+      tma_load_1d(s.inv, cb.inv, sizeof(s.inv), &s.tbar);
+    }
   }
-  for (int i = tid; i < 32 * 32; i += ENC_THREADS) (&s.mb[0][0])[i] = cb.mma_b[i];
   // ---- 1. gather the chunk's 64 stream rows (kvcache.py:179-186) ----------
   for (int i = tid; i < R * (D / 4); i += ENC_THREADS) {
     const int t = i / (D / 4), c4 = i - t * (D / 4);
@@ -274,171 +286,226 @@ __device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, i
     // token tt belongs to warp tt / 8, which also decides its sub-vectors below
     __syncwarp();
   }
-  // (b) tensor-core pre-pass: scores[sub][c] = u . e_c / ||e_c|| with u and
-  // the normalized entries split into fp16 hi + lo (three mma.sync m16n8k8:
-  // u_hi.e_hi + u_lo.e_hi + u_hi.e_lo).  One m-tile = the 16 sub-vectors of
-  // one token; warp w takes tokens 8w .. 8w+7.  Scores are tracked as packed
-  // (score bits | index c) keys with top-2 per sub-vector; a sub-vector whose runner-up is within the
-  // error bound is re-scored exactly in fp64 (the reference loop).
+  // (b) codebook search on the 5th-gen tensor cores.  A tile = the 128
+  // sub-vectors of 8 tokens (row r = token 8 tile + r / 16, sub r % 16).
+  // Thread r (and r + 128) writes row r of the A operand [u_hi | u_lo] (fp16
+  // split of u = |v| or v) to shared memory; one thread issues, per round,
+  //   D[r][j] = [u_hi | u_lo] . [e_hi | e_hi]_c + [u_hi | u_lo] . [e_lo | e_lo]_c
+  // (two tcgen05.mma, M = 128, N = ENC_NCOL, K = 16; c = ENC_NCOL round + j)
+  // into TMEM, i.e. u . e_c / ||e_c|| with an error below 2^-19 ||u||
+  // (fp16 hi + lo operands, fp32 accumulation).  Thread r (TMEM lane r)
+  // then scans its half of the columns in 32-column segments, two passes
+  // over the registers of one tcgen05.ld: the segment maximum m, then
+  // the count and position of the entries >= m - bound.  Segments merge by
+  // their maxima; a sub-vector whose best entry is not alone within `bound`
+  // (4 x 2^-17 ||u||, twice the pair error) is a near tie and is re-scored
+  // exactly in fp64 (the reference loop).  No top-2 tracking and no index
+  // packing: about 2.5 instructions per (sub-vector, entry).
+  mbar_wait(&s.tbar, 0);
   int slow = 0;
+  {
+    constexpr int ROUNDS = NENT / ENC_NCOL;
+    constexpr int NTILE = R / 8;
+    constexpr uint32_t IDESC = tc05::idesc_f16(128, ENC_NCOL);  // A, B K-major
+    const int r_row = tid & 127;   // A row written and TMEM lane read by this thread
+    const int chalf = tid >> 7;    // components 4 chalf.. of the A row / column half scanned
+    const uint32_t b_s = smem_u32(s.tcb);
+    const uint32_t t_lane = s.tmem_base + ((uint32_t)(32 * (warp & 3)) << 16);
+    uint32_t mma_phase = 0;
+    // A operand of tile `tile` into buffer `buf`: this thread converts
+    // components 4 chalf .. 4 chalf + 3 of row r_row into fp16 hi (K 0..7)
+    // and lo (K 8..15) halves; returns ||v||^2 of the row (fp32)
+    auto build_a = [&](int tile, int buf) -> float {
+      const int tau = 8 * tile + (r_row >> 4), sub = r_row & 15;
+      const float4 a = *reinterpret_cast<const float4 *>(&s.x[tau][8 * sub]);
+      const float4 b = *reinterpret_cast<const float4 *>(&s.x[tau][8 * sub + 4]);
+      float n2 = 0.f;
+      n2 = fmaf(a.x, a.x, n2); n2 = fmaf(a.y, a.y, n2); n2 = fmaf(a.z, a.z, n2); n2 = fmaf(a.w, a.w, n2);
+      n2 = fmaf(b.x, b.x, n2); n2 = fmaf(b.y, b.y, n2); n2 = fmaf(b.z, b.z, n2); n2 = fmaf(b.w, b.w, n2);
+      const float4 m = chalf ? b : a;
+      const float u0 = FOLD ? fabsf(m.x) : m.x, u1 = FOLD ? fabsf(m.y) : m.y;
+      const float u2 = FOLD ? fabsf(m.z) : m.z, u3 = FOLD ? fabsf(m.w) : m.w;
+      const __half2 h01 = __floats2half2_rn(u0, u1), h23 = __floats2half2_rn(u2, u3);
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+      const __half2 l01 = __floats2half2_rn(u0 - f01.x, u1 - f01.y);
+      const __half2 l23 = __floats2half2_rn(u2 - f23.x, u3 - f23.y);
+      const uint32_t dst = smem_u32(s.atile[buf]) +
+                           (uint32_t)((r_row >> 3) * 256 + (r_row & 7) * 16 + chalf * 8);
+      asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dst),
+                   "r"(*reinterpret_cast<const uint32_t *>(&h01)),
+                   "r"(*reinterpret_cast<const uint32_t *>(&h23)));
+      asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dst + 128u),
+                   "r"(*reinterpret_cast<const uint32_t *>(&l01)),
+                   "r"(*reinterpret_cast<const uint32_t *>(&l23)));
+      return n2;
+    };
+    auto issue = [&](int buf, int rnd) {
+      if (tid == 0) {
+        tc05::fence_after();
+        const uint64_t ad = tc05::smem_desc(smem_u32(s.atile[buf]), 128, 256);
+        const uint32_t bo = (uint32_t)rnd * (ENC_NCOL * 32);
+        tc05::mma_f16_ss(s.tmem_base, ad, tc05::smem_desc(b_s + bo, 128, 256), IDESC, 0);
+        tc05::mma_f16_ss(s.tmem_base, ad, tc05::smem_desc(b_s + NENT * 32 + bo, 128, 256), IDESC, 1);
+        tc05::commit(smem_u32(&s.mbar));
+      }
+    };
+    // scan this thread's columns of round `rnd` in 32-column segments
+    auto scan = [&](int rnd, float bound, float &M, int &bidx, bool &near) {
+      mbar_wait(&s.mbar, mma_phase);
+      mma_phase ^= 1u;
+      tc05::fence_after();
 #pragma unroll 1
-  for (int hf = 0; hf < 2; ++hf) {  // two passes of 4 tokens keep the live state small
-    uint32_t A[4][4];
+      for (int sg = 0; sg < ENC_NCOL / 64; ++sg) {
+        const int col0 = (ENC_NCOL / 2) * chalf + 32 * sg;
+        uint32_t xv[32];
+        tc05::ld_32x32b_x32(t_lane + (uint32_t)col0, xv);
+        tc05::wait_ld();
+        float mq[4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int tau = 8 * warp + 4 * hf + m;
-      const float2 v0 = *reinterpret_cast<const float2 *>(&s.x[tau][8 * g + 2 * lt]);
-      const float2 v1 = *reinterpret_cast<const float2 *>(&s.x[tau][8 * (g + 8) + 2 * lt]);
-      float u0 = FOLD ? fabsf(v0.x) : v0.x, u1 = FOLD ? fabsf(v0.y) : v0.y;
-      float w0 = FOLD ? fabsf(v1.x) : v1.x, w1 = FOLD ? fabsf(v1.y) : v1.y;
-      float h0, l0, h1, l1, h2, l2, h3, l3;
-      split_h(u0, h0, l0);
-      split_h(u1, h1, l1);
-      split_h(w0, h2, l2);
-      split_h(w1, h3, l3);
-      A[m][0] = pack_h2(h0, h1);  // row g   (sub g),   K cols 2t..2t+1: u_hi
-      A[m][1] = pack_h2(h2, h3);  // row g+8 (sub g+8)
-      A[m][2] = pack_h2(l0, l1);  // row g,   K cols 2t+8..2t+9: u_lo
-      A[m][3] = pack_h2(l2, l3);  // row g+8
-    }
-    // top-2 of packed keys: the score's fp32 bits with the low 8 mantissa bits
-    // replaced by the entry index (a perturbation below 2^-15 |score|, added
-    // to the near-tie bound), so max / min carry the index along
-    float best[4][2], sec[4][2];
+        for (int q = 0; q < 4; ++q) {
+          mq[q] = fmaxf(__uint_as_float(xv[q]), __uint_as_float(xv[q + 4]));
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+          for (int j = q + 8; j < 32; j += 8)
+            mq[q] = fmaxf(mq[q], fmaxf(__uint_as_float(xv[j]), __uint_as_float(xv[j + 4])));
+        }
+        const float m = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        const float thr = m - bound;
+        int ac2[2] = {0, 0};  // two chains: count << 8 | sum of positions
 #pragma unroll
-      for (int r = 0; r < 2; ++r) best[m][r] = sec[m][r] = -3.0e38f;
-#pragma unroll 2
-    for (int nt = 0; nt < 32; ++nt) {
-      // three m16n8k8 products u_hi.e_hi + u_lo.e_hi + u_hi.e_lo: each B
-      // operand is one register as loaded (no pair copies)
-      const uint2 bb = s.mb[nt][lane];
-      const uint32_t c0 = (uint32_t)(8 * nt + 2 * lt), c1 = c0 | 1u;
-#pragma unroll
-      for (int mp = 0; mp < 4; mp += 2) {  // two m-tiles interleaved: no back-to-back dependent MMAs
-      float dd[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-      for (int i = 0; i < 2; ++i) mma1688(dd[i], A[mp + i][0], A[mp + i][1], bb.x);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) mma1688(dd[i], A[mp + i][2], A[mp + i][3], bb.x);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) mma1688(dd[i], A[mp + i][0], A[mp + i][1], bb.y);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int m = mp + i;
-        const float(&d)[4] = dd[i];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const float a = __uint_as_float((__float_as_uint(d[2 * r]) & 0xffffff00u) | c0);
-          const float b = __uint_as_float((__float_as_uint(d[2 * r + 1]) & 0xffffff00u) | c1);
-          const float mx = fmaxf(a, b), mn = fminf(a, b);
-          sec[m][r] = fmaxf(sec[m][r], fmaxf(fminf(best[m][r], mx), mn));
-          best[m][r] = fmaxf(best[m][r], mx);
+        for (int j = 0; j < 32; ++j)  // one compare + one predicated add per entry
+          asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\t@p add.s32 %0, %0, %3;\n\t}"
+              : "+r"(ac2[j & 1])
+              : "f"(__uint_as_float(xv[j])), "f"(thr), "r"(256 + j));
+        const int acc = ac2[0] + ac2[1];
+        const bool nr = (acc >> 8) != 1;
+        const int ix = rnd * ENC_NCOL + col0 + (acc & 255);
+        if (m > M) {
+          near = nr || M >= m - bound;
+          M = m;
+          bidx = ix;
+        } else {
+          near = near || m >= M - bound;
         }
       }
-      }
-    }
-    // merge the top-2 lists of the four lanes sharing a sub-vector (same g)
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-#pragma unroll
-        for (int off = 1; off <= 2; off <<= 1) {
-          const float ob = __shfl_xor_sync(0xffffffffu, best[m][r], off);
-          const float os = __shfl_xor_sync(0xffffffffu, sec[m][r], off);
-          sec[m][r] = fmaxf(fminf(best[m][r], ob), fmaxf(sec[m][r], os));
-          best[m][r] = fmaxf(best[m][r], ob);
+    };
+
+    float n2 = build_a(0, 0);
+    tc05::fence_proxy_async();
+    __syncthreads();
+    issue(0, 0);
+#pragma unroll 1
+    for (int tile = 0; tile < NTILE; ++tile) {
+      const int buf = tile & 1;
+      const int tau = 8 * tile + (r_row >> 4), sub = r_row & 15;
+      const float bound = 3.0517578e-05f * sqrtf(n2);  // 4 x 2^-17 ||u||
+      float M = -INFINITY;
+      int bidx = 0;
+      bool near = false;
+      float n2_next = 0.f;
+#pragma unroll 1
+      for (int rnd = 0; rnd < ROUNDS; ++rnd) {
+        if (rnd) {
+          tc05::fence_before();
+          __syncthreads();  // every thread read the previous round's scores
+          issue(buf, rnd);
         }
+        if (rnd == ROUNDS - 1 && tile + 1 < NTILE) {  // next tile's A while the MMA runs
+          n2_next = build_a(tile + 1, buf ^ 1);
+          tc05::fence_proxy_async();
+        }
+        scan(rnd, bound, M, bidx, near);
       }
-    // decide: lane lt owns token m = lt of this pass (rows g and g + 8)
-    uint32_t need = 0;  // bit r: row r of this lane's token needs the exact pass
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      if (m != lt) continue;
-      const int tau = 8 * warp + 4 * hf + m;
-      const uint32_t zm = s.zmask[tau];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int sub = g + 8 * r;
+      s.rec[chalf][r_row] = make_float2(M, __int_as_float(bidx | (near ? 0x10000 : 0)));
+      tc05::fence_before();
+      __syncthreads();  // records complete; scores read; next A complete
+      if (tile + 1 < NTILE) issue(buf ^ 1, 0);  // next tile's first round under the merge
+      uint32_t need = 0;
+      if (tid < 128) {
+        const float2 A = s.rec[0][r_row], B = s.rec[1][r_row];
+        const int ia = __float_as_int(A.y), ib = __float_as_int(B.y);
+        bool nr;
+        int ix;
+        float best;
+        if (B.x > A.x) {
+          nr = (ib >> 16) || A.x >= B.x - bound;
+          ix = ib & 0xffff;
+          best = B.x;
+        } else {
+          nr = (ia >> 16) || B.x >= A.x - bound;
+          ix = ia & 0xffff;
+          best = A.x;
+        }
         uint8_t res = 0;
-        if (!((zm >> sub) & 1u)) {
-          const float sb = best[m][r], ss = sec[m][r];
-          float n2 = 0.f;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float v = s.x[tau][8 * sub + k];
-            n2 = fmaf(v, v, n2);
-          }
-          // fp16 hi + lo operands (2^-22 each) with fp32 tensor-core
-          // accumulation: |score error| < 2^-19 * ||u|| (4x margin: 2^-17),
-          // plus the index bits of both keys (< 2^-15 * ||u|| each)
-          const float bound = (2.0f * 7.6293945e-06f + 2.0f * 3.0517578e-05f) * sqrtf(n2);
-          if (n2 > 1e-24f && n2 < 1e30f && ss < sb - bound && fabsf(sb) > 1e-30f)
-            res = (uint8_t)(__float_as_uint(sb) & 0xffu);
+        if (!((s.zmask[tau] >> sub) & 1u)) {
+          if (n2 > 1e-24f && n2 < 1e30f && !nr && fabsf(best) > 1e-30f)
+            res = (uint8_t)ix;
           else
-            need |= 1u << r;
+            need = 1;
         }
         s.idx[tau][sub] = res;
       }
-    }
-    // near ties: the whole warp re-scores one sub-vector at a time exactly in
-    // fp64 (the reference loop: component-order sum, times inv[c], strict '>'
-    // from -1e300 so the lowest index wins ties); lane l scores entries
-    // l, l + 32, ..., then an argmax butterfly with the lower index on ties
-    for (uint32_t pend = __ballot_sync(0xffffffffu, need != 0); pend;
-         pend = __ballot_sync(0xffffffffu, need != 0)) {
-      const int src = __ffs(pend) - 1;
-      const uint32_t nb = __shfl_sync(0xffffffffu, need, src);
-      const int r = __ffs(nb) - 1;
-      const int tau = 8 * warp + 4 * hf + (src & 3), sub = (src >> 2) + 8 * r;
-      double ud[8];
+      // near ties: the whole warp re-scores one sub-vector at a time exactly
+      // in fp64 (the reference loop: component-order sum, times inv[c],
+      // strict '>' from -1e300 so the lowest index wins ties); lane l scores
+      // entries l, l + 32, ..., then an argmax butterfly, lower index on ties
+      if (warp < 4) {
+        for (uint32_t pend = __ballot_sync(0xffffffffu, need != 0); pend; pend &= pend - 1) {
+          const int src = __ffs(pend) - 1;
+          const int rr = 32 * warp + src;
+          const int tau2 = 8 * tile + (rr >> 4), sub2 = rr & 15;
+          double ud[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float v = s.x[tau][8 * sub + k];
-        ud[k] = (double)((FOLD && v < 0.f) ? -v : v);
-      }
-      double bs = -1e300;
-      int bc = 0;
+          for (int k = 0; k < 8; ++k) {
+            const float v = s.x[tau2][8 * sub2 + k];
+            ud[k] = (double)((FOLD && v < 0.f) ? -v : v);
+          }
+          double bs = -1e300;
+          int bc = 0;
 #pragma unroll 2
-      for (int i = 0; i < NENT / 32; ++i) {
-        const int c = 32 * i + lane;
-        const float4 e0 = *reinterpret_cast<const float4 *>(&s.ent[8 * c]);
-        const float4 e1 = *reinterpret_cast<const float4 *>(&s.ent[8 * c + 4]);
-        double sc = __dmul_rn(ud[0], (double)e0.x);
-        sc = __dadd_rn(sc, __dmul_rn(ud[1], (double)e0.y));
-        sc = __dadd_rn(sc, __dmul_rn(ud[2], (double)e0.z));
-        sc = __dadd_rn(sc, __dmul_rn(ud[3], (double)e0.w));
-        sc = __dadd_rn(sc, __dmul_rn(ud[4], (double)e1.x));
-        sc = __dadd_rn(sc, __dmul_rn(ud[5], (double)e1.y));
-        sc = __dadd_rn(sc, __dmul_rn(ud[6], (double)e1.z));
-        sc = __dadd_rn(sc, __dmul_rn(ud[7], (double)e1.w));
-        sc = __dmul_rn(sc, s.inv[c]);
-        if (sc > bs) {
-          bs = sc;
-          bc = c;
-        }
-      }
+          for (int i = 0; i < NENT / 32; ++i) {
+            const int c = 32 * i + lane;
+            const float4 e0 = *reinterpret_cast<const float4 *>(&s.ent[8 * c]);
+            const float4 e1 = *reinterpret_cast<const float4 *>(&s.ent[8 * c + 4]);
+            double sc = __dmul_rn(ud[0], (double)e0.x);
+            sc = __dadd_rn(sc, __dmul_rn(ud[1], (double)e0.y));
+            sc = __dadd_rn(sc, __dmul_rn(ud[2], (double)e0.z));
+            sc = __dadd_rn(sc, __dmul_rn(ud[3], (double)e0.w));
+            sc = __dadd_rn(sc, __dmul_rn(ud[4], (double)e1.x));
+            sc = __dadd_rn(sc, __dmul_rn(ud[5], (double)e1.y));
+            sc = __dadd_rn(sc, __dmul_rn(ud[6], (double)e1.z));
+            sc = __dadd_rn(sc, __dmul_rn(ud[7], (double)e1.w));
+            sc = __dmul_rn(sc, s.inv[c]);
+            if (sc > bs) {
+              bs = sc;
+              bc = c;
+            }
+          }
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, bs, off);
-        const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
-        if (os > bs || (os == bs && oc < bc)) {
-          bs = os;
-          bc = oc;
+          for (int off = 16; off >= 1; off >>= 1) {
+            const double os = __shfl_xor_sync(0xffffffffu, bs, off);
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, off);
+            if (os > bs || (os == bs && oc < bc)) {
+              bs = os;
+              bc = oc;
+            }
+          }
+          if (lane == src) {
+            s.idx[tau2][sub2] = (uint8_t)bc;
+            ++slow;
+          }
         }
       }
-      if (lane == src) {
-        s.idx[tau][sub] = (uint8_t)bc;
-        need &= ~(1u << r);
-        ++slow;
-      }
+      n2 = n2_next;
     }
   }
   if (slow) atomicAdd(&s.cnt[NSNKV_CNT_NEARTIE], slow);
   if (clamps) atomicAdd(&s.cnt[NSNKV_CNT_CLAMP], clamps);
+  tc05::fence_before();
   __syncthreads();
+  if (warp == 0) {
+    tc05::fence_after();
+    tc05::dealloc(s.tmem_base, ENC_NCOL);
+  }
 
   // ---- 5. scale adjustment (vq.py:74-93, 249-254) --------------------------
   {
