@@ -108,17 +108,13 @@ __device__ __forceinline__ float4 warp_fwht128(float4 v) {
     const float oy = __shfl_xor_sync(0xffffffffu, v.y, m);
     const float oz = __shfl_xor_sync(0xffffffffu, v.z, m);
     const float ow = __shfl_xor_sync(0xffffffffu, v.w, m);
-    if (lane & m) {  // this lane holds the "y" half
-      v.x = __fsub_rn(ox, v.x);
-      v.y = __fsub_rn(oy, v.y);
-      v.z = __fsub_rn(oz, v.z);
-      v.w = __fsub_rn(ow, v.w);
-    } else {
-      v.x = __fadd_rn(v.x, ox);
-      v.y = __fadd_rn(v.y, oy);
-      v.z = __fadd_rn(v.z, oz);
-      v.w = __fadd_rn(v.w, ow);
-    }
+    // the "y" half (lane & m) takes o - v, the "x" half v + o: one FMA with
+    // an exact +-1 product is the same single rounding as the add / sub
+    const float sg = (lane & m) ? -1.0f : 1.0f;
+    v.x = __fmaf_rn(sg, v.x, ox);
+    v.y = __fmaf_rn(sg, v.y, oy);
+    v.z = __fmaf_rn(sg, v.z, oz);
+    v.w = __fmaf_rn(sg, v.w, ow);
   }
   const float sc = 0.08838834764831845f;  // float32(1/sqrt(128))
   v.x = __fmul_rn(v.x, sc);
@@ -202,16 +198,22 @@ __device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, i
     }
   }
   // ---- 1. gather the chunk's 64 stream rows (kvcache.py:179-186) ----------
-  for (int i = tid; i < R * (D / 4); i += ENC_THREADS) {
-    const int t = i / (D / 4), c4 = i - t * (D / 4);
-    const int64_t srow = (int64_t)k * R + t;
-    float4 v;
-    if (srow < J.n_resid) {
-      v = *reinterpret_cast<const float4 *>(J.res + srow * D + 4 * c4);
-    } else {
-      v = load_row4(J.fresh, (srow - J.n_resid) * J.fresh_stride + 4 * c4, J.fresh_bf16);
+  // (every load of the thread issued before the first store: one exposed
+  // memory latency per chunk)
+  {
+    const int c4 = tid & 31;
+    float4 v[R * (D / 4) / ENC_THREADS];
+#pragma unroll
+    for (int n = 0; n < R * (D / 4) / ENC_THREADS; ++n) {
+      const int t = (tid >> 5) + (ENC_THREADS / 32) * n;
+      const int64_t srow = (int64_t)k * R + t;
+      v[n] = srow < J.n_resid ? *reinterpret_cast<const float4 *>(J.res + srow * D + 4 * c4)
+                              : load_row4(J.fresh, (srow - J.n_resid) * J.fresh_stride + 4 * c4,
+                                          J.fresh_bf16);
     }
-    *reinterpret_cast<float4 *>(&s.x[t][4 * c4]) = v;
+#pragma unroll
+    for (int n = 0; n < R * (D / 4) / ENC_THREADS; ++n)
+      *reinterpret_cast<float4 *>(&s.x[(tid >> 5) + (ENC_THREADS / 32) * n][4 * c4]) = v[n];
   }
   __syncthreads();
   if (J.res_dst) {  // the unit's new residual rows (its old ones are in s.x now)
@@ -370,13 +372,13 @@ __device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, i
         }
         const float m = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         const float thr = m - bound;
-        int ac2[2] = {0, 0};  // two chains: count << 8 | sum of positions
+        int ac2[4] = {0, 0, 0, 0};  // four chains: count << 8 | sum of positions
 #pragma unroll
         for (int j = 0; j < 32; ++j)  // one compare + one predicated add per entry
           asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\t@p add.s32 %0, %0, %3;\n\t}"
-              : "+r"(ac2[j & 1])
+              : "+r"(ac2[j & 3])
               : "f"(__uint_as_float(xv[j])), "f"(thr), "r"(256 + j));
-        const int acc = ac2[0] + ac2[1];
+        const int acc = (ac2[0] + ac2[1]) + (ac2[2] + ac2[3]);
         const bool nr = (acc >> 8) != 1;
         const int ix = rnd * ENC_NCOL + col0 + (acc & 255);
         if (m > M) {
