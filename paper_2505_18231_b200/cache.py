@@ -50,21 +50,23 @@ def default_precision(bit_mode) -> str:
     fp16 key codeword (11-bit significand) puts a relative error of ~2^-12 on
     every score, and with large-magnitude scores (outlier tokens) that shifts
     the softmax far beyond the 1e-3 output tolerance (2-bit misaligned data,
-    4K context: 3e-2).  Value codewords may be plain fp16 in
-    2-bit mode ("vfast": the per-component signs make the rounding errors
-    cancel, <= 2.5e-4 at 32K context), but not in 1-bit mode, where the
-    unsigned codewords accumulate a bias that grows with the context (1.5e-3
-    at 4K, 3.7e-3 at 32K), so 1-bit decodes "precise"."""
-    return "vfast" if int(bit_mode) == 2 else "precise"
+    4K context: 3e-2).  Value codewords are plain fp16 in both
+    bit modes ("vfast").  2-bit: the per-component signs make the rounding
+    errors cancel (<= 2.5e-4 at 32K context).  1-bit: the unsigned codewords'
+    rounding errors have a nonzero mean that would accumulate with the context
+    (1.7e-3 at 4K, 4.0e-3 at 32K uncorrected); the kernel adds the codebook's
+    mean rounding error times the summed weights (CodebookDev::dbar), which
+    leaves 2.6e-4 at 4K and at 32K."""
+    return "vfast"
 
 
 def check_precision(precision: str, bit_mode, allow_inexact: bool = False) -> str:
-    """Validate a precision mode for a bit mode.  Modes that are known to
-    exceed the 1e-3 output tolerance on some inputs ("fast" in either bit
-    mode, "vfast" in 1-bit mode) need an explicit allow_inexact=True."""
+    """Validate a precision mode for a bit mode.  "fast" (plain-fp16 key
+    codewords) is known to exceed the 1e-3 output tolerance on outlier data
+    and needs an explicit allow_inexact=True."""
     if precision not in PRECISIONS:
         raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
-    inexact = precision == "fast" or (precision == "vfast" and int(bit_mode) == 1)
+    inexact = precision == "fast"
     if inexact and not allow_inexact:
         raise Unsupported(f"precision {precision!r} exceeds the 1e-3 output tolerance on some "
                           f"{int(bit_mode)}-bit inputs; pass allow_inexact=True to use it")

@@ -102,6 +102,14 @@ extern "C" int nsnkv_codebook_create(const float *entries_host, const double *in
   }
   nsnkv_codebook *cb = new nsnkv_codebook();
   cb->dev.bit_mode = bit_mode;
+  for (int k = 0; k < 8; ++k) {  // mean fp16 rounding error of component k
+    double acc = 0.0;
+    for (int c = 0; c < NENT; ++c) {
+      const float x = entries_host[8 * c + k];
+      acc += (double)x - (double)__half2float(__float2half_rn(x));
+    }
+    cb->dev.dbar[k] = (float)(acc / NENT);
+  }
   cudaError_t err = cudaSuccess;
   err = cudaMalloc(&cb->dev.entries, NENT * 8 * sizeof(float));
   if (!err) err = cudaMalloc(&cb->dev.inv, NENT * sizeof(double));

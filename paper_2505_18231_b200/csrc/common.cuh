@@ -59,6 +59,12 @@ struct CodebookDev {
   // no-swizzle K-major canonical layout: byte (c / 8) * 256 + khalf * 128 +
   // (c % 8) * 16.
   uint4 *tcb;
+  // mean over the 256 entries of the fp16 rounding error e - fp16(e), per
+  // component: decode with plain-fp16 value codewords adds
+  // (sum of the chunk weights) x dbar to every sub-vector of the output, so
+  // the unsigned (1-bit) codewords' rounding leaves no bias that grows with
+  // the context
+  float dbar[8];
   int bit_mode;
 };
 

@@ -192,6 +192,9 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int CP = C::CP, NTP = C::NTP, NGRP = C::NGRP, NSTAGE = C::NSTAGE;
   constexpr bool HILO_K = PREC <= 1;  // precise (0) and vfast (1): fp16 hi + lo key codewords
   constexpr bool HILO_V = PREC == 0;  // precise only: fp16 hi + lo value codewords
+  // plain-fp16 unsigned (1-bit) value codewords: add (sum of P') x dbar per
+  // sub-vector at the end of a unit (the codebook's mean rounding error)
+  constexpr bool VBIAS = !FOLD && !HILO_V;
   constexpr PageLayout L = page_layout(FOLD ? 2 : 1);
   constexpr uint32_t PB = (uint32_t)C::PAGE;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -613,6 +616,8 @@ __global__ void __launch_bounds__(512, 1)
     uint32_t qB[NTP][8][2];
     float accV[NTP][8][4];
     float m_run[NTP], l_run[NTP];
+    float pv_run[NTP];  // VBIAS: running sum of P' = p s1 s2 (this lane's tokens)
+    const float dbar_g = VBIAS ? cv.cb_v.dbar[g] : 0.f;  // channels 16 mt + g (+ 8)
 
     auto write_empty = [&](int unit) {
       if (ws == 0 && lane < G) {
@@ -624,7 +629,7 @@ __global__ void __launch_bounds__(512, 1)
     // merge the 4 warps' partials in a fixed order (3, 2, 1, 0) through one
     // [G][D] buffer; warp 0 writes the record
     auto flush_unit = [&](int unit) {
-      float lw[NTP];
+      float lw[NTP], cor[NTP];
 #pragma unroll
       for (int nt = 0; nt < NTP; ++nt) {
         float l = l_run[nt];
@@ -632,6 +637,14 @@ __global__ void __launch_bounds__(512, 1)
         l += __shfl_xor_sync(0xffffffffu, l, 8);
         l += __shfl_xor_sync(0xffffffffu, l, 16);
         lw[nt] = l;
+        cor[nt] = 0.f;
+        if (VBIAS) {
+          float pv = pv_run[nt];
+          pv += __shfl_xor_sync(0xffffffffu, pv, 4);
+          pv += __shfl_xor_sync(0xffffffffu, pv, 8);
+          pv += __shfl_xor_sync(0xffffffffu, pv, 16);
+          cor[nt] = pv * dbar_g;
+        }
       }
       named_bar(bar_id, 128);
       for (int r = 3; r >= 0; --r) {
@@ -656,8 +669,8 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
               for (int mt = 0; mt < 8; ++mt) {
                 const int c = 16 * mt + g;  // accumulator rows g / g + 8 of m-tile mt
-                float a0 = (accV[nt][mt][0] + accV[nt][mt][1]) * sa;
-                float a1 = (accV[nt][mt][2] + accV[nt][mt][3]) * sa;
+                float a0 = (accV[nt][mt][0] + accV[nt][mt][1] + cor[nt]) * sa;
+                float a1 = (accV[nt][mt][2] + accV[nt][mt][3] + cor[nt]) * sa;
                 if (r < 3) {
                   a0 = fmaf(S.mg.acc[h][c], sb, a0);
                   a1 = fmaf(S.mg.acc[h][c + 8], sb, a1);
@@ -672,8 +685,8 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
               for (int mt = 0; mt < 8; ++mt) {
                 const int c = 16 * mt + g;
-                rec[4 + c] = fmaf(S.mg.acc[h][c], sb, (accV[nt][mt][0] + accV[nt][mt][1]) * sa);
-                rec[4 + c + 8] = fmaf(S.mg.acc[h][c + 8], sb, (accV[nt][mt][2] + accV[nt][mt][3]) * sa);
+                rec[4 + c] = fmaf(S.mg.acc[h][c], sb, (accV[nt][mt][0] + accV[nt][mt][1] + cor[nt]) * sa);
+                rec[4 + c + 8] = fmaf(S.mg.acc[h][c + 8], sb, (accV[nt][mt][2] + accV[nt][mt][3] + cor[nt]) * sa);
               }
               if (g == 0) {
                 rec[0] = m;
@@ -743,6 +756,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         m_run[nt] = -INFINITY;
         l_run[nt] = 0.f;
+        pv_run[nt] = 0.f;
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
@@ -898,6 +912,7 @@ __global__ void __launch_bounds__(512, 1)
         if (m_new > m_run[nt]) {
           const float rr = exp2f(m_run[nt] - m_new);
           l_run[nt] *= rr;
+          if (VBIAS) pv_run[nt] *= rr;
 #pragma unroll
           for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
@@ -909,6 +924,7 @@ __global__ void __launch_bounds__(512, 1)
           float p0 = exp2f(x[c][0] - m_new), p1 = exp2f(x[c][1] - m_new);
           if (h >= G || c >= cnt) p0 = p1 = 0.f;
           l_run[nt] += p0 + p1;
+          if (VBIAS) pv_run[nt] = fmaf(p1, sct[c][1].z, fmaf(p0, sct[c][0].z, pv_run[nt]));
           float ws2 = p0 * sct[c][0].w + p1 * sct[c][1].w;
           ws2 += __shfl_xor_sync(0xffffffffu, ws2, 4);
           ws2 += __shfl_xor_sync(0xffffffffu, ws2, 8);

@@ -116,7 +116,7 @@ def test_gpu_c1_decode_vs_reference_and_exact(case):
     import torch
 
     g = load_golden(f"c1_{case['name']}.npz")
-    modes = ["precise"] + (["vfast"] if case["bit_mode"] == 2 else [])
+    modes = ["precise", "vfast"]
     q = torch.from_numpy(case["q"].reshape(1, -1, 128)).cuda()
     for prec in modes:
         c = _gpu_cache(case, precision=prec)

@@ -54,11 +54,15 @@ def _build(B, Hkv, T, mode, seed, append_block=4096, precision="precise"):
     ("2b", 16, 32, 8, 32768, "vfast"),      # BASELINE config 2 (headline, default mode)
     ("2b", 4, 32, 8, 32768, "precise"),
     ("1b", 4, 32, 8, 32768 + 37, "precise"),  # 1-bit with a residual tail
+    ("1b", 4, 32, 8, 32768 + 37, "vfast"),    # 1-bit default: fp16 values + mean-error term
     ("2b", 2, 8, 8, 4096 + 5, "vfast"),     # G = 1 (config 1 geometry)
     ("1b", 1, 8, 8, 4096, "precise"),       # config 1 itself
+    ("1b", 1, 8, 8, 4096, "vfast"),
     ("2b", 3, 16, 2, 1000, "vfast"),        # G = 8, ragged
     ("2b", 3, 16, 2, 1000, "precise"),
     ("1b", 2, 4, 2, 64 * 3, "precise"),     # G = 2
+    ("1b", 2, 4, 2, 64 * 3, "vfast"),
+    ("1b", 3, 16, 2, 1000, "vfast"),        # G = 8, 1-bit
 ])
 def test_fused_decode_vs_oracle(mode, B, Hq, Hkv, T, precision):
     import torch

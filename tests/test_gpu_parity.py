@@ -159,9 +159,9 @@ def test_fused_precision_modes_vs_reference(case):
 
     g = load_golden(f"pipeline_{case['name']}.npz")
     cb = codebook_for(case["bit_mode"])
-    # key codewords are always hi + lo; 2-bit may use plain fp16 value
-    # codewords ("vfast"), 1-bit may not (cache.default_precision)
-    modes = ("precise",) + (("vfast",) if cb.bit_mode == 2 else ())
+    # key codewords are always hi + lo; value codewords may be plain fp16
+    # ("vfast") in both bit modes (cache.default_precision)
+    modes = ("precise", "vfast")
     for prec in modes:
         cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode, strategy=P.ScaleStrategy(case["strategy"]))
         c = P.PagedKvCache(cfg, 1, 1, cb_k=cb, cb_v=cb, base_position=case["base_position"],

@@ -121,7 +121,8 @@ def test_decode_c2_all_units_vs_oracle(c2_cache, precision):
     assert err.max() <= TOL, (precision, err.max(), np.unravel_index(err.argmax(), err.shape))
 
 
-@pytest.mark.parametrize("mode,precision", [("2b", "vfast"), ("2b", "precise"), ("1b", "precise")])
+@pytest.mark.parametrize("mode,precision", [("2b", "vfast"), ("2b", "precise"), ("1b", "precise"),
+                                            ("1b", "vfast")])
 def test_decode_misaligned_long_context_vs_oracle(mode, precision):
     """Outlier tokens make scores large, so every relative error on a score
     is amplified by the softmax: the key codewords must carry ~22 bits

@@ -227,10 +227,11 @@ def test_precision_policy():
     from paper_2505_18231_b200.cache import PRECISIONS, check_precision, default_precision
     from paper_2505_18231_b200.errors import Unsupported
 
-    assert default_precision(2) == "vfast" and default_precision(1) == "precise"
+    assert default_precision(2) == "vfast" and default_precision(1) == "vfast"
     assert check_precision("precise", 1) == "precise"
     assert check_precision("vfast", 2) == "vfast"
-    for prec, bm in (("fast", 2), ("fast", 1), ("vfast", 1)):
+    assert check_precision("vfast", 1) == "vfast"
+    for prec, bm in (("fast", 2), ("fast", 1)):
         with pytest.raises(Unsupported):
             check_precision(prec, bm)
         assert check_precision(prec, bm, allow_inexact=True) == prec
