@@ -191,6 +191,12 @@ __global__ void __launch_bounds__(512, 1)
   using C = A3<G, FOLD, PREC>;
   constexpr int CP = C::CP, NTP = C::NTP, NGRP = C::NGRP, NSTAGE = C::NSTAGE;
   constexpr bool HILO_K = PREC <= 1;  // precise (0) and vfast (1): fp16 hi + lo key codewords
+  // 3 (1-bit, G = 4): key side by a per-unit lookup table in shared memory,
+  // LUT[c][j] = (<HT(q_h)_j, e_c>, h = 0..3) in fp32, built by the consumers
+  // at every unit change of the CTA's range (all groups step through the
+  // units together); values as in vfast
+  constexpr bool LUTK = PREC == 3;
+  static_assert(!LUTK || (G == 4 && !FOLD), "the key lookup table is built for 1-bit, G = 4");
   constexpr bool HILO_V = PREC == 0;  // precise only: fp16 hi + lo value codewords
   // plain-fp16 unsigned (1-bit) value codewords: add (sum of P') x dbar per
   // sub-vector at the end of a unit (the codebook's mean rounding error)
@@ -246,8 +252,8 @@ __global__ void __launch_bounds__(512, 1)
       mbar_init(&BR.tabs, C::ONE_TABLE ? 128 : 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       if (!C::ONE_TABLE) {
-        mbar_expect_tx(&BR.tabs, 2 * 65536);
-        tma_load_1d(smem + (tab_k - base), cv.cb_k.tabw, 65536, &BR.tabs);
+        mbar_expect_tx(&BR.tabs, LUTK ? 65536 : 2 * 65536);
+        if (!LUTK) tma_load_1d(smem + (tab_k - base), cv.cb_k.tabw, 65536, &BR.tabs);
         tma_load_1d(smem + (tab_v - base), cv.cb_v.tabw, 65536, &BR.tabs);
       }
     }
@@ -619,6 +625,69 @@ __global__ void __launch_bounds__(512, 1)
     float pv_run[NTP];  // VBIAS: running sum of P' = p s1 s2 (this lane's tokens)
     const float dbar_g = VBIAS ? cv.cb_v.dbar[g] : 0.f;  // channels 16 mt + g (+ 8)
 
+    // LUTK: entry c, sub j at byte c * 256 + lut_slot(j) * 16 of the K table
+    // region: the 8 lanes of a quarter-warp (g = 2q, 2q + 1; t = 0..3) read
+    // subs 4 t + m and 4 t + (m ^ 2), whose slots fall in 8 different bank
+    // groups, so every LDS.128 phase is conflict-free
+    auto lut_slot = [](int j) -> uint32_t { return (uint32_t)((j & 8) | ((j + (j >> 3)) & 7)); };
+    uint32_t lutb[4], lsel[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int mm = (g & 1) ? (m ^ 2) : m;
+      lutb[m] = tab_k | (lut_slot(4 * t + mm) << 4);
+      lsel[m] = 0x7604u | ((uint32_t)mm << 4);
+    }
+    auto lut_transition = [&](int U) {
+      named_bar(4, 384);  // every consumer is done with the previous unit's table
+      if (grp == 0) {     // HT(q_h) of the unit's G = 4 q-heads (warp ws: head ws)
+        const int b = U / cv.n_kv_heads, hk = U - b * cv.n_kv_heads;
+        const float *qs = qg + ((int64_t)b * cv.n_q_heads + (int64_t)hk * G + ws) * D;
+        float4 v = *reinterpret_cast<const float4 *>(qs + 4 * lane);
+        float a = v.x + v.y, bq = v.x - v.y, c = v.z + v.w, d = v.z - v.w;
+        v.x = a + c; v.z = a - c; v.y = bq + d; v.w = bq - d;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+          const float ox = __shfl_xor_sync(0xffffffffu, v.x, m);
+          const float oy = __shfl_xor_sync(0xffffffffu, v.y, m);
+          const float oz = __shfl_xor_sync(0xffffffffu, v.z, m);
+          const float ow = __shfl_xor_sync(0xffffffffu, v.w, m);
+          if (lane & m) {
+            v.x = ox - v.x; v.y = oy - v.y; v.z = oz - v.z; v.w = ow - v.w;
+          } else {
+            v.x += ox; v.y += oy; v.z += oz; v.w += ow;
+          }
+        }
+        const float sc = 0.08838834764831845f;
+        v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+        *reinterpret_cast<float4 *>(&CS[0].su.qh[ws][4 * lane]) = v;
+      }
+      named_bar(4, 384);
+      {  // thread i: sub j = i % 16, entries c = i / 16 + 24 k
+        const int i = 128 * grp + ci, j = i & 15;
+        float qv[4][8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) qv[h][k] = CS[0].su.qh[h][8 * j + k];
+        const uint32_t sl = lut_slot(j) << 4;
+        const float4 *ent = reinterpret_cast<const float4 *>(cv.cb_k.entries);
+        for (int c = i >> 4; c < NENT; c += 24) {
+          const float4 e0 = __ldg(ent + 2 * c), e1 = __ldg(ent + 2 * c + 1);
+          float r[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            float x = qv[h][0] * e0.x;
+            x = fmaf(qv[h][1], e0.y, x); x = fmaf(qv[h][2], e0.z, x); x = fmaf(qv[h][3], e0.w, x);
+            x = fmaf(qv[h][4], e1.x, x); x = fmaf(qv[h][5], e1.y, x); x = fmaf(qv[h][6], e1.z, x);
+            r[h] = fmaf(qv[h][7], e1.w, x);
+          }
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(tab_k + (uint32_t)c * 256u + sl),
+                       "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]));
+        }
+      }
+      named_bar(4, 384);  // table complete
+    };
+
     auto write_empty = [&](int unit) {
       if (ws == 0 && lane < G) {
         float *rec = record_ptr<G>(recs, (unit + blockIdx.x) * NGRP + grp);
@@ -771,6 +840,8 @@ __global__ void __launch_bounds__(512, 1)
     int mark_next = first_unit;
     int n = 0;
     mbar_wait(&BR.tabs, 0);
+    int lut_unit = first_unit;
+    if (LUTK) lut_transition(first_unit);
 
     for (int k = grp; cur.x < hi; k += NGRP, ++n) {
       if (cur.u != cur_unit) {
@@ -780,6 +851,8 @@ __global__ void __launch_bounds__(512, 1)
         }
         for (int u = mark_next; u < cur.u; ++u) write_empty(u);
         mark_next = cur.u;
+        if (LUTK)
+          while (lut_unit < cur.u) lut_transition(++lut_unit);
         setup_unit(cur.u);
         cur_unit = cur.u;
       }
@@ -798,7 +871,37 @@ __global__ void __launch_bounds__(512, 1)
         // fast mode computes a missing second chunk on stale stage bytes
         // (gathers only ever return finite table entries; its weights are
         // masked to zero) so both chunks' gathers can interleave
-        if (C::ONE_TABLE || c < cnt) {
+        if (LUTK) {
+          if (c < cnt) {
+            const uint32_t kpa = smem_u32(st + c * 2 * C::MAIN);
+            const uint32_t ik0 = lds32(kpa + L.idx + tok0 * NSUB + 4 * t);
+            const uint32_t ik1 = lds32(kpa + L.idx + tok1 * NSUB + 4 * t);
+            float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const uint4 w0 = lds128(prmt(ik0, lutb[m], lsel[m]));
+              const uint4 w1 = lds128(prmt(ik1, lutb[m], lsel[m]));
+              a0[0] += __uint_as_float(w0.x); a0[1] += __uint_as_float(w0.y);
+              a0[2] += __uint_as_float(w0.z); a0[3] += __uint_as_float(w0.w);
+              a1[0] += __uint_as_float(w1.x); a1[1] += __uint_as_float(w1.y);
+              a1[2] += __uint_as_float(w1.z); a1[3] += __uint_as_float(w1.w);
+            }
+            // sum the 4 lanes t of a token, lane t keeping head t: heads
+            // (t & 2, +1) over xor 2, then head t over xor 1
+            const bool hb = t & 2, lb = t & 1;
+            float k0 = hb ? a0[2] : a0[0], k1 = hb ? a0[3] : a0[1];
+            float k2 = hb ? a1[2] : a1[0], k3 = hb ? a1[3] : a1[1];
+            k0 += __shfl_xor_sync(0xffffffffu, hb ? a0[0] : a0[2], 2);
+            k1 += __shfl_xor_sync(0xffffffffu, hb ? a0[1] : a0[3], 2);
+            k2 += __shfl_xor_sync(0xffffffffu, hb ? a1[0] : a1[2], 2);
+            k3 += __shfl_xor_sync(0xffffffffu, hb ? a1[1] : a1[3], 2);
+            float v0 = lb ? k1 : k0, v1 = lb ? k3 : k2;
+            v0 += __shfl_xor_sync(0xffffffffu, lb ? k0 : k1, 1);
+            v1 += __shfl_xor_sync(0xffffffffu, lb ? k2 : k3, 1);
+            pd[c][0][0] = v0;
+            pd[c][0][1] = v1;
+          }
+        } else if (C::ONE_TABLE || c < cnt) {
           const uint32_t kpa = smem_u32(st + c * 2 * C::MAIN);
           const uint32_t ik0 = lds32(kpa + L.idx + tok0 * NSUB + 4 * t);
           const uint32_t ik1 = lds32(kpa + L.idx + tok1 * NSUB + 4 * t);
@@ -1011,6 +1114,8 @@ __global__ void __launch_bounds__(512, 1)
       mark_next = cur_unit + 1;
     }
     for (int u = mark_next; u <= last_unit; ++u) write_empty(u);
+    if (LUTK)
+      while (lut_unit < last_unit) lut_transition(++lut_unit);
   }
 
   tc05::fence_before();
@@ -1057,3 +1162,4 @@ NSNKV_A3_INST_G(1)
 NSNKV_A3_INST_G(2)
 NSNKV_A3_INST_G(4)
 NSNKV_A3_INST_G(8)
+NSNKV_A3_INST(4, false, 3)

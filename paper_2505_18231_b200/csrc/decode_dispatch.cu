@@ -86,6 +86,11 @@ static int decode_attend(const nsnkv_cache_view *cv_in, const float *q, float *o
 #define NSNKV_ATT(GG)         \
   if (fold) NSNKV_ATT_P(GG, true); \
   else NSNKV_ATT_P(GG, false)
+  // 1-bit, G = 4, values in fp16: the key side by lookup table when the
+  // CTAs' chunk ranges are long enough to amortise the per-unit table build
+  if (!fold && G == 4 && prec == 1 && total >= 32 * (int64_t)attend_grid() &&
+      !std::getenv("NSNKV_NO_LUT"))
+    return launch_attend<4, false, 3>(cv, q, out, lse, recs, total, st, add);
   switch (G) {
     case 1: NSNKV_ATT(1);
     case 2: NSNKV_ATT(2);
