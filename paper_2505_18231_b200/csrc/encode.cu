@@ -53,41 +53,69 @@ struct EncodeSmem {
   uint32_t tmem_base;
 };
 
-// fp64 sum of squares of one token row held 4-per-lane (lane l owns
-// elements 4l..4l+3): lane partial ((a0+a1)+a2)+a3, then an xor butterfly
-// 16, 8, 4, 2, 1.  The oracle restates exactly this order.
-__device__ __forceinline__ double warp_row_sumsq(float4 v) {
-  double p = (double)v.x * (double)v.x;
-  p = __dadd_rn(p, (double)v.y * (double)v.y);
-  p = __dadd_rn(p, (double)v.z * (double)v.z);
-  p = __dadd_rn(p, (double)v.w * (double)v.w);
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, off));
-  return p;
-}
-
 // _scale_per_token (nsn.py:58-65) on every row of s.x; returns clamps.
+// Warp w owns rows w + 8 i (i = 0..7), lane l elements 4l..4l+3 of each.
+// The fp64 sum of squares follows exactly the order of warp_row_sumsq (lane
+// partial, then the xor tree 16, 8, 4, 2, 1; the oracle restates it), but
+// the eight rows are reduced together by recursive halving: at each level a
+// lane keeps half of its rows and adds the partner's partials of them (the
+// same pairwise sums as the butterfly), so after three levels lane l holds
+// row (l >> 2)'s tree and the norm, scale and clamp are computed once per
+// row.  The division v / sc is exact: RN32((double)v * RN64(1 / sc)) is
+// RN32(v / sc) because the fp64 product is within 2^-52 of the quotient and a
+// quotient of two binary32 numbers is never closer than 2^-49 (relative) to a
+// binary32 rounding boundary.
 __device__ int scale_rows(EncodeSmem &s, float *scale_out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float sqrt_d = 11.313708498984761f;  // float32(sqrt(128))
-  int clamps = 0;
-  for (int t = warp; t < R; t += ENC_THREADS / 32) {
-    float4 v = *reinterpret_cast<float4 *>(&s.x[t][4 * lane]);
-    const double ss = warp_row_sumsq(v);
-    const float nrm = __fsqrt_rn(__double2float_rn(ss));  // row_norms, core.py:50-53
-    float sc = __fdiv_rn(nrm, sqrt_d);
-    if (sc < 1e-8f) {  // NORM_EPS clamp, nsn.py:61-64
-      sc = 1e-8f;
-      ++clamps;
-    }
-    v.x = __fdiv_rn(v.x, sc);
-    v.y = __fdiv_rn(v.y, sc);
-    v.z = __fdiv_rn(v.z, sc);
-    v.w = __fdiv_rn(v.w, sc);
-    *reinterpret_cast<float4 *>(&s.x[t][4 * lane]) = v;
-    if (lane == 0) scale_out[t] = sc;
+  constexpr int NR = R / (ENC_THREADS / 32);  // 8 rows per warp
+  float4 v[NR];
+  double p[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    v[i] = *reinterpret_cast<float4 *>(&s.x[warp + 8 * i][4 * lane]);
+    const double a = v[i].x, b = v[i].y, c = v[i].z, d = v[i].w;
+    double q = a * a;  // products of binary32 values are exact in fp64
+    q = __fma_rn(b, b, q);
+    q = __fma_rn(c, c, q);
+    p[i] = __fma_rn(d, d, q);
   }
-  return lane == 0 ? clamps : 0;
+  const int bA = (lane >> 4) & 1, bB = (lane >> 3) & 1, bC = (lane >> 2) & 1;
+  double q4[4], q2[2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double keep = bA ? p[4 + k] : p[k], send = bA ? p[k] : p[4 + k];
+    q4[k] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double keep = bB ? q4[2 + k] : q4[k], send = bB ? q4[k] : q4[2 + k];
+    q2[k] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+  }
+  double ss = __dadd_rn(bC ? q2[1] : q2[0], __shfl_xor_sync(0xffffffffu, bC ? q2[0] : q2[1], 4));
+  ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 2));
+  ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 1));
+  // this lane's row: i* = 4 bA + 2 bB + bC (= lane >> 2)
+  const float nrm = __fsqrt_rn(__double2float_rn(ss));  // row_norms, core.py:50-53
+  float sc = __fdiv_rn(nrm, sqrt_d);
+  int clamps = 0;
+  if (sc < 1e-8f) {  // NORM_EPS clamp, nsn.py:61-64
+    sc = 1e-8f;
+    clamps = (lane & 3) == 0 ? 1 : 0;
+  }
+  if ((lane & 3) == 0) scale_out[warp + 8 * (lane >> 2)] = sc;
+  const double y = __drcp_rn((double)sc);
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const double yi = __shfl_sync(0xffffffffu, y, 4 * i);
+    float4 w = v[i];
+    w.x = __double2float_rn(__dmul_rn((double)w.x, yi));
+    w.y = __double2float_rn(__dmul_rn((double)w.y, yi));
+    w.z = __double2float_rn(__dmul_rn((double)w.z, yi));
+    w.w = __double2float_rn(__dmul_rn((double)w.w, yi));
+    *reinterpret_cast<float4 *>(&s.x[warp + 8 * i][4 * lane]) = w;
+  }
+  return clamps;
 }
 
 // In-warp FWHT of one 128-row held 4-per-lane (fp32 add/sub only), then the
