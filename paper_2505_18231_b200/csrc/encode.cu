@@ -45,8 +45,8 @@ struct EncodeSmem {
   float s1[R], s2[R], o[D];
   uint16_t zmask[R];              // zero sub-vectors per token (bit j)
   float s2adj[R];
-  uint8_t idx[R][NSUB];
-  uint8_t sgn[R][NSUB];
+  __align__(16) uint8_t idx[R][NSUB];
+  __align__(16) uint8_t sgn[R][NSUB];
   int cnt[NSNKV_NUM_COUNTERS];
   uint64_t mbar;                  // tcgen05.commit -> search rounds
   uint64_t tbar;                  // bulk copies of the codebook tables
@@ -544,18 +544,23 @@ __device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, i
     for (int t0 = warp * 4; t0 < R; t0 += (ENC_THREADS / 32) * 4) {
       const int t = t0 + slot;
       double v2 = 0.0, q2 = 0.0, dt = 0.0;
-#pragma unroll 4
+      const uint4 iw = *reinterpret_cast<const uint4 *>(&s.idx[t][0]);
+      const uint4 sw = *reinterpret_cast<const uint4 *>(&s.sgn[t][0]);
+      const uint32_t iws[4] = {iw.x, iw.y, iw.z, iw.w}, sws[4] = {sw.x, sw.y, sw.z, sw.w};
+#pragma unroll
       for (int i = 0; i < NSUB; ++i) {  // element 8i + j; numpy pairwise_sum order
         const float v = s.x[t][8 * i + j];
-        float c = s.ent[s.idx[t][i] * 8 + j];
-        if (fold && ((s.sgn[t][i] >> j) & 1)) c = -c;  // _SIGN_LUT, codebook.py:49
+        const uint32_t ci = (iws[i >> 2] >> (8 * (i & 3))) & 0xffu;
+        float c = s.ent[ci * 8 + j];
+        if (fold)  // _SIGN_LUT, codebook.py:49: flip where sign bit j of the byte is set
+          c = __uint_as_float(__float_as_uint(c) ^ (((sws[i >> 2] >> (8 * (i & 3) + j)) & 1u) << 31));
         const double vd = (double)v, cd = (double)c;
-        if (i == 0) {
+        if (i == 0) {  // products of binary32 values are exact in fp64: fma == mul + add
           v2 = vd * vd; q2 = cd * cd; dt = vd * cd;
         } else {
-          v2 = __dadd_rn(v2, vd * vd);
-          q2 = __dadd_rn(q2, cd * cd);
-          dt = __dadd_rn(dt, vd * cd);
+          v2 = __fma_rn(vd, vd, v2);
+          q2 = __fma_rn(cd, cd, q2);
+          dt = __fma_rn(vd, cd, dt);
         }
       }
 #pragma unroll
