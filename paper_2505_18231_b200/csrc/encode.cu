@@ -42,7 +42,8 @@ struct EncodeSmem {
   __align__(16) float ent[NENT * 8];
   double inv[NENT];
   float2 rec[2][128];             // per column half: best score, index | near-tie flag
-  float s1[R], s2[R], o[D];
+  float s1[R], s2[R];
+  __align__(16) float o[D];
   uint16_t zmask[R];              // zero sub-vectors per token (bit j)
   float s2adj[R];
   __align__(16) uint8_t idx[R][NSUB];
@@ -53,7 +54,8 @@ struct EncodeSmem {
   uint32_t tmem_base;
 };
 
-// _scale_per_token (nsn.py:58-65) on every row of s.x; returns clamps.
+// _scale_per_token (nsn.py:58-65) on every row of s.x (minus `shift` per
+// column when given); returns clamps.
 // Warp w owns rows w + 8 i (i = 0..7), lane l elements 4l..4l+3 of each.
 // The fp64 sum of squares follows exactly the order of warp_row_sumsq (lane
 // partial, then the xor tree 16, 8, 4, 2, 1; the oracle restates it), but
@@ -65,7 +67,7 @@ struct EncodeSmem {
 // RN32(v / sc) because the fp64 product is within 2^-52 of the quotient and a
 // quotient of two binary32 numbers is never closer than 2^-49 (relative) to a
 // binary32 rounding boundary.
-__device__ int scale_rows(EncodeSmem &s, float *scale_out) {
+__device__ int scale_rows(EncodeSmem &s, float *scale_out, const float *shift = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float sqrt_d = 11.313708498984761f;  // float32(sqrt(128))
   constexpr int NR = R / (ENC_THREADS / 32);  // 8 rows per warp
@@ -74,6 +76,13 @@ __device__ int scale_rows(EncodeSmem &s, float *scale_out) {
 #pragma unroll
   for (int i = 0; i < NR; ++i) {
     v[i] = *reinterpret_cast<float4 *>(&s.x[warp + 8 * i][4 * lane]);
+    if (shift) {  // column shift first (the rows are rewritten below)
+      const float4 o4 = *reinterpret_cast<const float4 *>(shift + 4 * lane);
+      v[i].x = __fsub_rn(v[i].x, o4.x);
+      v[i].y = __fsub_rn(v[i].y, o4.y);
+      v[i].z = __fsub_rn(v[i].z, o4.z);
+      v[i].w = __fsub_rn(v[i].w, o4.w);
+    }
     const double a = v[i].x, b = v[i].y, c = v[i].z, d = v[i].w;
     double q = a * a;  // products of binary32 values are exact in fp64
     q = __fma_rn(b, b, q);
@@ -261,12 +270,7 @@ __device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, i
     s.o[tid] = __double2float_rn(__ddiv_rn(acc, (double)R));
   }
   __syncthreads();
-  for (int i = tid; i < R * D; i += ENC_THREADS) {
-    const int t = i / D, c = i - t * D;
-    s.x[t][c] = __fsub_rn(s.x[t][c], s.o[c]);
-  }
-  __syncthreads();
-  clamps += scale_rows(s, s.s2);
+  clamps += scale_rows(s, s.s2, s.o);  // v_ns = v_n - o (nsn.py:80), then s2
   __syncthreads();
 
   // ---- 3. keys: RoPE at absolute positions, then FWHT (kvcache.py:121-123)
