@@ -1,7 +1,7 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck /
 synccheck): ragged appends (nsnkv_append), fused decode (attend3 + combine),
 the fused serving step (nsnkv_decode_step), unfused decode, snapshot import,
-the codebook-build passes and the level-1 kernels."""
+the 1-bit key-table decode, the codebook-build passes and the level-1 kernels."""
 import sys
 from pathlib import Path
 
@@ -35,6 +35,18 @@ for mode, G, prec in (("2b", 4, "vfast"), ("2b", 4, "precise"), ("1b", 1, None),
     d.attend(q)
     torch.cuda.synchronize()
     print(mode, G, c.precision, float((out - out2).abs().max()))
+# 1-bit, G = 4, >= 32 chunks per CTA: the key-side lookup-table decode
+# (per-unit table builds behind named barriers, several units per CTA)
+cb = P.default_codebook("1b")
+cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
+B, H, T = 8, 8, 64 * 80
+c = P.PagedKvCache(cfg, B, H, max_tokens=T, cb_k=cb, cb_v=cb, check_finite=False)
+x = torch.randn(B, H, T, 128, device="cuda")
+c.append(x, x)
+q = torch.randn(B, H * 4, 128, device="cuda")
+c.attend(q)
+torch.cuda.synchronize()
+print("1b lut", c.precision, c.n_chunks)
 rng = np.random.Generator(np.random.PCG64(0))
 CB.kmeans_init(rng, "2b", n_samples=4096, n_iters=2)
 v = np.random.default_rng(0).standard_normal((3000, 8)).astype(np.float32)
