@@ -88,6 +88,7 @@ struct A3 {
     uint64_t full[24], empty[24];
     uint64_t ready[NGRP][NSLOT], free_[NGRP][NSLOT];
     uint64_t tabs;
+    uint64_t zdone[NGRP];  // the group's shift-term MMA chain finished reading Z
     uint32_t tmem_base;
   };
   static constexpr int BARS = ((int)sizeof(Bars) + 127) / 128 * 128;
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(512, 1)
           mbar_init(&BR.free_[q][s], 128);  // every consumer thread of the group
         }
       mbar_init(&BR.tabs, C::ONE_TABLE ? 128 : 1);
+      for (int q = 0; q < NGRP; ++q) mbar_init(&BR.zdone[q], 1);  // one commit per chain
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       if (!C::ONE_TABLE) {
         mbar_expect_tx(&BR.tabs, LUTK ? 65536 : 2 * 65536);
@@ -502,7 +504,8 @@ __global__ void __launch_bounds__(512, 1)
         const int m = n / BATCH, e = n % BATCH;
         if (m >= NZB) {
           const int n0 = (m - NZB) * BATCH;
-          mbar_wait(&BR.ready[gp][n0 % NSLOT], (uint32_t)((n0 / NSLOT) & 1));
+          (void)n0;
+          mbar_wait(&BR.zdone[gp], (uint32_t)((m - NZB) & 1));
         }
         const uint32_t zb_s = smem_u32(P.zb[m % NZB]);
         // Z (MN-major B operand): element (k, n) at (k/8)*256 + (n/8)*128 +
@@ -583,6 +586,7 @@ __global__ void __launch_bounds__(512, 1)
                                tc05::smem_desc(zb_s + (uint32_t)(kt * NB * 32), NB * 16, 128), idesc,
                                kt > 0);
             for (int q = nf; q <= n; ++q) tc05::commit(smem_u32(&BR.ready[gp][q % NSLOT]));
+            tc05::commit(smem_u32(&BR.zdone[gp]));
           }
         }
         __syncwarp();
@@ -638,6 +642,7 @@ __global__ void __launch_bounds__(512, 1)
       lsel[m] = 0x7604u | ((uint32_t)mm << 4);
     }
     auto lut_transition = [&](int U) {
+      __syncwarp();       // converged warps at the (aligned) named barrier
       named_bar(4, 384);  // every consumer is done with the previous unit's table
       if (grp == 0) {     // HT(q_h) of the unit's G = 4 q-heads (warp ws: head ws)
         const int b = U / cv.n_kv_heads, hk = U - b * cv.n_kv_heads;
@@ -840,22 +845,14 @@ __global__ void __launch_bounds__(512, 1)
     int mark_next = first_unit;
     int n = 0;
     mbar_wait(&BR.tabs, 0);
-    int lut_unit = first_unit;
-    if (LUTK) lut_transition(first_unit);
-
-    for (int k = grp; cur.x < hi; k += NGRP, ++n) {
-      if (cur.u != cur_unit) {
-        if (cur_unit >= 0) {
-          flush_unit(cur_unit);
-          mark_next = cur_unit + 1;
-        }
-        for (int u = mark_next; u < cur.u; ++u) write_empty(u);
-        mark_next = cur.u;
-        if (LUTK)
-          while (lut_unit < cur.u) lut_transition(++lut_unit);
-        setup_unit(cur.u);
-        cur_unit = cur.u;
-      }
+    // units of the CTA's range in order; with the key table every group runs
+    // every unit's transition from this one call site (named barriers)
+    // with the key table, the units of the CTA's range are walked in order
+    // and every group runs each unit's table transition from this one call
+    // site (named barriers), flushing its own partials of a unit first;
+    // otherwise one pass over the group's items
+    // one work item (CP chunks of unit cur.u) of this consumer group
+    auto process_item = [&]() {
       const int cnt = item3_count<CP>(cur);
       const int s = grp * C::NS + n % C::NS, slot = n % C::NSLOT;
       mbar_wait(&BR.full[s], (uint32_t)(n / C::NS) & 1u);
@@ -1107,6 +1104,22 @@ __global__ void __launch_bounds__(512, 1)
       tc05::fence_before();
       mbar_arrive(&BR.empty[s]);
       mbar_arrive(&BR.free_[grp][slot]);
+    };
+
+    if constexpr (!LUTK) {
+    for (;; ++n) {
+      if (!(cur.x < hi)) break;
+      if (cur.u != cur_unit) {
+        if (cur_unit >= 0) {
+          flush_unit(cur_unit);
+          mark_next = cur_unit + 1;
+        }
+        for (int u = mark_next; u < cur.u; ++u) write_empty(u);
+        mark_next = cur.u;
+        setup_unit(cur.u);
+        cur_unit = cur.u;
+      }
+      process_item();
       for (int a = 0; a < NGRP; ++a) item3_next<CP>(cur, hi, cv.n_chunks, n_units);
     }
     if (cur_unit >= 0) {
@@ -1114,8 +1127,30 @@ __global__ void __launch_bounds__(512, 1)
       mark_next = cur_unit + 1;
     }
     for (int u = mark_next; u <= last_unit; ++u) write_empty(u);
-    if (LUTK)
-      while (lut_unit < last_unit) lut_transition(++lut_unit);
+    } else {
+    int lut_unit = first_unit - 1;  // last unit whose table transition this group ran
+    for (;; ++n) {
+      const bool have = cur.x < hi;
+      const int next_u = have ? cur.u : last_unit + 1;
+      if (next_u != cur_unit) {  // unit change (or the end of the range)
+        if (cur_unit >= 0) {
+          flush_unit(cur_unit);
+          mark_next = cur_unit + 1;
+        }
+        for (int u = mark_next; u < next_u && u <= last_unit; ++u) write_empty(u);
+        mark_next = next_u;
+        // every group runs every unit's table transition, from this one call
+        // site (named barriers), the skipped and the trailing units included
+        if (LUTK)
+          while (lut_unit < (next_u <= last_unit ? next_u : last_unit)) lut_transition(++lut_unit);
+        if (!have) break;
+        setup_unit(cur.u);
+        cur_unit = cur.u;
+      }
+      process_item();
+      for (int a = 0; a < NGRP; ++a) item3_next<CP>(cur, hi, cv.n_chunks, n_units);
+    }
+    }
   }
 
   tc05::fence_before();
