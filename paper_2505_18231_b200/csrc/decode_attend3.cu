@@ -447,8 +447,10 @@ __global__ void __launch_bounds__(512, 1)
         if (n >= NSLOT) mbar_wait(&BR.free_[gp][slot], (uint32_t)((n / NSLOT) - 1) & 1u);
         // stage the item's page tails; field offsets are relative to the tail
         __syncwarp();
-        *reinterpret_cast<uint4 *>(P.tails + 32 * lane) = tl0[0];
-        *reinterpret_cast<uint4 *>(P.tails + 32 * lane + 16) = tl0[1];
+        if (lane < 16 * CP) {  // 8 lanes per tail, K and V tail per chunk (TAILS bytes)
+          *reinterpret_cast<uint4 *>(P.tails + 32 * lane) = tl0[0];
+          *reinterpret_cast<uint4 *>(P.tails + 32 * lane + 16) = tl0[1];
+        }
         __syncwarp();
         const uint8_t *st = P.tails;
         // tail field offsets (the page layout's minus the payload size)

@@ -35,6 +35,25 @@ for mode, G, prec in (("2b", 4, "vfast"), ("2b", 4, "precise"), ("1b", 1, None),
     d.attend(q)
     torch.cuda.synchronize()
     print(mode, G, c.precision, float((out - out2).abs().max()))
+# multi-item CTAs (~13 chunks per CTA: several work items per consumer group,
+# producers reusing their shift-term operand) in every gather-path mode,
+# with fused serving steps
+for mode, G, prec in (("2b", 4, "vfast"), ("2b", 4, "precise"), ("1b", 4, "precise"),
+                      ("2b", 8, "vfast"), ("1b", 2, "vfast"), ("2b", 1, "vfast")):
+    cb = P.default_codebook(mode)
+    cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
+    B, H, T = 4, 8, 64 * 60 + 5
+    c = P.PagedKvCache(cfg, B, H, max_tokens=T + 8, cb_k=cb, cb_v=cb, precision=prec,
+                       check_finite=False)
+    x = torch.randn(B, H, T, 128, device="cuda")
+    c.append(x, x)
+    q = torch.randn(B, H * G, 128, device="cuda")
+    c.attend(q)
+    for _ in range(2):
+        tok = torch.randn(B, H, 1, 128, device="cuda")
+        c.decode_step(q, tok, tok)
+    torch.cuda.synchronize()
+    print("multi-item", mode, G, c.precision)
 # 1-bit, G = 4, >= 32 chunks per CTA: the key-side lookup-table decode
 # (per-unit table builds behind named barriers, several units per CTA)
 cb = P.default_codebook("1b")

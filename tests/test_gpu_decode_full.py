@@ -59,6 +59,9 @@ def _build(B, Hkv, T, mode, seed, append_block=4096, precision="precise"):
     ("1b", 1, 8, 8, 4096, "precise"),       # config 1 itself
     ("1b", 1, 8, 8, 4096, "vfast"),
     ("2b", 3, 16, 2, 1000, "vfast"),        # G = 8, ragged
+    ("2b", 2, 64, 8, 4096 + 5, "vfast"),    # G = 8, several work items per CTA (one-chunk items)
+    ("1b", 2, 64, 8, 4096 + 5, "vfast"),
+    ("2b", 2, 64, 8, 4096 + 5, "precise"),
     ("2b", 3, 16, 2, 1000, "precise"),
     ("1b", 2, 4, 2, 64 * 3, "precise"),     # G = 2
     ("1b", 2, 4, 2, 64 * 3, "vfast"),
