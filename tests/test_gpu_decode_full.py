@@ -38,7 +38,7 @@ def _build(B, Hkv, T, mode, seed, append_block=4096, precision="precise"):
     cb = P.default_codebook(mode)
     cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
     cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, check_finite=False,
-                           precision=precision)
+                           precision=precision, allow_inexact=precision == "fast")
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
     done = 0
@@ -64,6 +64,9 @@ def _build(B, Hkv, T, mode, seed, append_block=4096, precision="precise"):
     ("2b", 2, 64, 8, 4096 + 5, "precise"),
     ("2b", 3, 16, 2, 1000, "precise"),
     ("1b", 2, 4, 2, 64 * 3, "precise"),     # G = 2
+    ("1b", 2, 16, 8, 4096 + 5, "vfast"),    # G = 2, several work items per CTA
+    ("2b", 2, 16, 8, 4096 + 5, "precise"),
+    ("2b", 4, 32, 8, 8192 + 3, "fast"),     # opt-in fp16 mode (N(0,1) data), paired items
     ("1b", 2, 4, 2, 64 * 3, "vfast"),
     ("1b", 3, 16, 2, 1000, "vfast"),        # G = 8, 1-bit
 ])
