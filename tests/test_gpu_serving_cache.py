@@ -164,17 +164,17 @@ def test_decode_step_launches_and_no_host_sync():
     assert c.unit_n_chunks.tolist() == [3] * 32 and c.unit_n_res.tolist() == [4] * 32
 
 
-@pytest.mark.parametrize("mode,G", [("2b", 4), ("1b", 8), ("2b", 1)])
-def test_decode_step_equals_append_then_attend(mode, G):
+@pytest.mark.parametrize("mode,G,B,H,nch", [("2b", 4, 2, 4, 2), ("1b", 8, 2, 4, 2), ("2b", 1, 2, 4, 2),
+                                            ("1b", 4, 8, 8, 80)])  # the last: key-table decode
+def test_decode_step_equals_append_then_attend(mode, G, B, H, nch):
     """The fused serving step (new rows attended and stored by the combine
     kernel) gives exactly the state and output of append + attend, across a
     chunk boundary (where it falls back to nsnkv_append)."""
-    B, H = 2, 4
     a = _cache(int(mode[0]), B, H, check_finite=False)
     b = _cache(int(mode[0]), B, H, check_finite=False)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(21)
-    x = torch.randn(B, H, 64 * 2 + 55, 128, device="cuda", generator=gen)
+    x = torch.randn(B, H, 64 * nch + 55, 128, device="cuda", generator=gen)
     a.append(x, x)
     b.append(x, x)
     for i in range(12):
@@ -185,6 +185,6 @@ def test_decode_step_equals_append_then_attend(mode, G):
         b.append(k, v)
         o2 = b.attend(q)
         assert torch.equal(o1, o2), i
-    assert a.unit_n_res.tolist() == b.unit_n_res.tolist() and a.unit_n_chunks[0] == 3
+    assert a.unit_n_res.tolist() == b.unit_n_res.tolist() and a.unit_n_chunks[0] == nch + 1
     for u in range(B * H):
         assert a.snapshot(u) == b.snapshot(u)
