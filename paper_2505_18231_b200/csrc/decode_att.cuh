@@ -247,6 +247,9 @@ __global__ void __launch_bounds__(COMBINE_THREADS) combine_kernel(
     *reinterpret_cast<float4 *>(&S.q[h][4 * lane]) =
         *reinterpret_cast<const float4 *>(qg + (int64_t)row * D + 4 * lane);
     // ---- stream-K records of the unit -----------------------------------
+    // (launched as a programmatic dependent of the attend kernel: the staging
+    // above overlaps its tail; its records are complete and visible here)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     int64_t off = 0;  // global chunk offset of unit u
     for (int uu = lane; uu < u; uu += 32) off += cv.n_chunks[uu];
 #pragma unroll

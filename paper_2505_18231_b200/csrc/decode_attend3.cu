@@ -264,6 +264,9 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   tc05::fence_after();
   const uint32_t tmem = BR.tmem_base;
+  // the combine kernel (programmatic dependent) may be scheduled as SMs free
+  // up; it waits for this grid's completion before it reads the records
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp >= 12) {
     // ======================= producer warpgroup ================================
@@ -1180,9 +1183,22 @@ int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, flo
     attend3_kernel<G, FOLD, PREC><<<grid, 512, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
     ++launches;
   }
-  combine_kernel<G, 3, true><<<cv.batch * cv.n_kv_heads, COMBINE_THREADS, sizeof(CombineSmem), st>>>(
-      cv, q, recs, total > 0 ? total : 1, grid, out, lse, add.k, add.v, add.bf16, add.n,
-      add.n_res_out);
+  {  // programmatic dependent launch: the combine CTAs start (residual rows,
+     // RoPE) while the attend kernel drains, then wait for its records
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(cv.batch * cv.n_kv_heads));
+    lc.blockDim = dim3(COMBINE_THREADS);
+    lc.dynamicSmemBytes = sizeof(CombineSmem);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = total > 0 ? 1 : 0;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, combine_kernel<G, 3, true>, cv, q, (const float *)recs,
+                       (int64_t)(total > 0 ? total : 1), grid, out, lse, add.k, add.v, add.bf16,
+                       add.n, add.n_res_out);
+  }
   ++launches;
   nsnkv_internal_count_launch(launches);
   return nsnkv_internal_check_launch("decode_attend");
