@@ -305,7 +305,12 @@ __device__ __forceinline__ void encode_chunk(EncodeSmem &s, const ChunkSrc &J, i
       const float4 b = *reinterpret_cast<float4 *>(&s.x[tt][8 * (j0 + i) + 4]);
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
       v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-      const bool zero = sq_norm8_pairwise(v) < 1e-24;
+      // codebook.py:118-120 zero test; a component of magnitude >= 1e-11 puts
+      // the (nonnegative, monotonically rounded) fp64 sum of squares above
+      // 1e-22, so the exact pairwise sum is only needed below that
+      float mx = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[4]), fabsf(v[5])), fmaxf(fabsf(v[6]), fabsf(v[7]))));
+      const bool zero = !(mx >= 1e-11f) && sq_norm8_pairwise(v) < 1e-24;
       const uint32_t sb = fold_signs(v, u, FOLD);
       s.sgn[tt][j0 + i] = zero ? 0 : (uint8_t)sb;
       zm |= (zero ? 1u : 0u) << (j0 + i);
