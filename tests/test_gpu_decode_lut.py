@@ -74,7 +74,8 @@ def test_lut_ragged_units_vs_oracle():
     B, Hkv, G, T = 64, 8, 4, 64 * 20
     cb = P.default_codebook("1b")
     cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
-    cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, check_finite=False)
+    cache = P.PagedKvCache(cfg, B, Hkv, max_tokens=T, cb_k=cb, cb_v=cb, check_finite=False,
+                           base_position=1000)  # RoPE positions offset (shift term)
     assert cache.precision == "vfast"
     g = torch.Generator(device="cuda")
     g.manual_seed(41)
