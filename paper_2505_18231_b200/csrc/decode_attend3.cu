@@ -159,27 +159,6 @@ __device__ __forceinline__ void item3_next(Item3 &it, int64_t hi, const int32_t 
   }
 }
 
-__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
 // rtn4_dequant (vq.py:133-136): zero + level * scale, two fp32 roundings
 __device__ __forceinline__ float rtn4(uint32_t level, float zero, float scale) {
   return __fadd_rn(zero, __fmul_rn((float)level, scale));
