@@ -7,8 +7,9 @@
 //   score_t = s1_t * ( s2_t * <HT(q), c_t> + <q, RoPE(o, p0 + tau)> )
 //   out     = FWHT( sum_t softmax_t * s1_t * (s2_t * c'_t + o') )
 //
-// Roles (512 threads, one CTA per SM, stream-K split of the chunk list into
-// work items of CP consecutive chunks of one unit):
+// Roles (512 threads -- 384 for GQA-8, see A3::NGRP -- one CTA per SM,
+// stream-K split of the chunk list into work items of CP consecutive chunks
+// of one unit):
 //  * warp 12 (TMA): streams each item's K and V page payloads, in item order,
 //    into its group's shared-memory ring with 1-D bulk copies
 //    (cp.async.bulk + mbarrier complete_tx);
@@ -44,8 +45,12 @@ template <int G, bool FOLD, int PREC>
 struct A3 {
   static constexpr int CP = G <= 4 ? 2 : 1;        // chunks per work item
   static constexpr int NTP = (2 * G + 7) / 8;      // payload n-tiles: (head, hi/lo) columns
-  static constexpr int NGRP = 3;                   // consumer groups
-  static constexpr int THREADS = 512;
+  // consumer groups of 4 warps (GQA-8: two, so the 8-head accumulators get
+  // the registers of a 384-thread CTA), then the producer warpgroup: warp
+  // CW streams pages, CW + 1 .. CW + NGRP produce items
+  static constexpr int NGRP = G == 8 ? 2 : 3;
+  static constexpr int CW = 4 * NGRP;
+  static constexpr int THREADS = 32 * (CW + 4);
   static constexpr int PAGE = FOLD ? NSNKV_PAGE_BYTES_2B : NSNKV_PAGE_BYTES_1B;
   // pages split in two streams: the payload (idx [+ signs]) for the consumer
   // groups, the 256-byte tail (s2, s1 / o nibbles, RTN-4 params) for the
@@ -165,7 +170,7 @@ __device__ __forceinline__ float rtn4(uint32_t level, float zero, float scale) {
 }
 
 template <int G, bool FOLD, int PREC>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(A3<G, FOLD, PREC>::THREADS, 1)
     attend3_kernel(CacheViewDev cv, const float *__restrict__ qg, float *__restrict__ recs,
                    int64_t total_chunks) {
   using C = A3<G, FOLD, PREC>;
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(512, 1)
   const int last_unit = cursor_seek(hi - 1, cv.n_chunks, n_units).u;
 
   // ---- set-up: barriers, TMEM, tables --------------------------------------
-  if (warp == 12) {
+  if (warp == C::CW) {
     tc05::alloc(smem_u32(&BR.tmem_base), C::TMEM_COLS);
     tc05::relinquish();
     if (lane == 0) {
@@ -247,11 +252,11 @@ __global__ void __launch_bounds__(512, 1)
   // up; it waits for this grid's completion before it reads the records
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  if (warp >= 12) {
+  if (warp >= C::CW) {
     // ======================= producer warpgroup ================================
-    const int pq = warp - 12;  // TMEM lane quarter of this warp
+    const int pq = warp - C::CW;  // TMEM lane quarter of this warp (CW is a multiple of 4)
     if (C::ONE_TABLE) {        // interleave the K and V hi gather tables
-      const int t128 = tid - 384;
+      const int t128 = tid - 32 * C::CW;
       const uint4 *sk = reinterpret_cast<const uint4 *>(cv.cb_k.tabw);
       const uint4 *sv = reinterpret_cast<const uint4 *>(cv.cb_v.tabw);
       uint4 *dst = reinterpret_cast<uint4 *>(smem + (tab_k - base));
@@ -290,8 +295,8 @@ __global__ void __launch_bounds__(512, 1)
     tc05::fence_after();
 
     constexpr int NSLOT = C::NSLOT, NZB = C::NZB;
-    if (warp == 12) {
-      // ---------------- warp 12: page streaming ---------------------------------
+    if (warp == C::CW) {
+      // ---------------- warp CW: page streaming ---------------------------------
       // payload (idx [+ signs]) of every item, in item order, into its group's
       // ring (NS stages per group) with 1-D bulk copies (TMA engine).  Page ids
       // come from 32-entry windows of the page table loaded by all lanes at
@@ -330,9 +335,9 @@ __global__ void __launch_bounds__(512, 1)
           item3_next<CP>(tit, hi, cv.n_chunks, n_units);
         }
       }
-    } else {
+    } else if (warp - C::CW - 1 < NGRP) {
       // ---------------- item producer of group gp ------------------------------
-      const int gp = warp - 13;
+      const int gp = warp - C::CW - 1;
       typename C::Prod &P = prod_of(gp);
       constexpr int HPR = CP == 2 ? G : 8;  // heads per Z row pair (CP = 1: two 4-head rows)
       Item3 it = start;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(512, 1)
     }
     auto lut_transition = [&](int U) {
       __syncwarp();       // converged warps at the (aligned) named barrier
-      named_bar(4, 384);  // every consumer is done with the previous unit's table
+      named_bar(4, 32 * C::CW);  // every consumer is done with the previous unit's table
       if (grp == 0) {     // HT(q_h) of the unit's G = 4 q-heads (warp ws: head ws)
         const int b = U / cv.n_kv_heads, hk = U - b * cv.n_kv_heads;
         const float *qs = qg + ((int64_t)b * cv.n_q_heads + (int64_t)hk * G + ws) * D;
@@ -650,7 +655,7 @@ __global__ void __launch_bounds__(512, 1)
         v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
         *reinterpret_cast<float4 *>(&CS[0].su.qh[ws][4 * lane]) = v;
       }
-      named_bar(4, 384);
+      named_bar(4, 32 * C::CW);
       {  // thread i: sub j = i % 16, entries c = i / 16 + 24 k
         const int i = 128 * grp + ci, j = i & 15;
         float qv[4][8];
@@ -660,7 +665,7 @@ __global__ void __launch_bounds__(512, 1)
           for (int k = 0; k < 8; ++k) qv[h][k] = CS[0].su.qh[h][8 * j + k];
         const uint32_t sl = lut_slot(j) << 4;
         const float4 *ent = reinterpret_cast<const float4 *>(cv.cb_k.entries);
-        for (int c = i >> 4; c < NENT; c += 24) {
+        for (int c = i >> 4; c < NENT; c += 2 * C::CW) {
           const float4 e0 = __ldg(ent + 2 * c), e1 = __ldg(ent + 2 * c + 1);
           float r[4];
 #pragma unroll
@@ -674,7 +679,7 @@ __global__ void __launch_bounds__(512, 1)
                        "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]));
         }
       }
-      named_bar(4, 384);  // table complete
+      named_bar(4, 32 * C::CW);  // table complete
     };
 
     auto write_empty = [&](int unit) {
@@ -1139,7 +1144,7 @@ __global__ void __launch_bounds__(512, 1)
 
   tc05::fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == C::CW) {
     tc05::fence_after();
     tc05::dealloc(tmem, C::TMEM_COLS);
   }
@@ -1156,10 +1161,11 @@ int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, flo
                          const AppendRows &add) {
   static unsigned long long attr = 0, attr_c = 0;
   set_smem_attr_once(attend3_kernel<G, FOLD, PREC>, ATT_SMEM_BYTES, attr);
-  set_smem_attr_once(combine_kernel<G, 3, true>, (int)sizeof(CombineSmem), attr_c);
+  using C = A3<G, FOLD, PREC>;
+  set_smem_attr_once(combine_kernel<G, C::NGRP, true>, (int)sizeof(CombineSmem), attr_c);
   int launches = 0;
   if (total > 0) {
-    attend3_kernel<G, FOLD, PREC><<<grid, 512, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
+    attend3_kernel<G, FOLD, PREC><<<grid, C::THREADS, ATT_SMEM_BYTES, st>>>(cv, q, recs, total);
     ++launches;
   }
   {  // programmatic dependent launch: the combine CTAs start (residual rows,
@@ -1174,7 +1180,7 @@ int nsnkv_launch_attend3(const CacheViewDev &cv, const float *q, float *out, flo
     at[0].val.programmaticStreamSerializationAllowed = total > 0 ? 1 : 0;
     lc.attrs = at;
     lc.numAttrs = 1;
-    cudaLaunchKernelEx(&lc, combine_kernel<G, 3, true>, cv, q, (const float *)recs,
+    cudaLaunchKernelEx(&lc, combine_kernel<G, C::NGRP, true>, cv, q, (const float *)recs,
                        (int64_t)(total > 0 ? total : 1), grid, out, lse, add.k, add.v, add.bf16,
                        add.n, add.n_res_out);
   }
