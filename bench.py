@@ -406,7 +406,7 @@ def run_ours(args) -> dict | None:
         del cache
         torch.cuda.empty_cache()
         if args.config == "c2":
-            for name in ("c2_1b", "c4"):
+            for name in ("c2_1b", "c4", "c2_g8"):
                 extras[name] = measure_config(name, device, peak, steps=max(10, args.steps // 5))
         res["extras"] = extras
         res["encode"] = {f"{m}b": measure_encode(device, m) for m in (2, 1)}
