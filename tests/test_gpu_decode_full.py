@@ -127,3 +127,30 @@ def test_decode_is_deterministic(mode, B, Hq, Hkv, T, precision):
     a = cache.attend(q).clone()
     for _ in range(10):
         assert torch.equal(a, cache.attend(q))
+
+
+def test_decode_c4_full_size_vs_oracle():
+    """BASELINE config 4 at full size on one GPU (batch 128 x 8 KV heads x
+    128K tokens, 2-bit, 32 q-heads per sequence: 9.6 GB of pages): sampled
+    units, first / middle / last, against the oracle on the GPU's own pages."""
+    import torch
+
+    B, Hq, Hkv, T = 128, 32, 8, 131072
+    cache = _build(B, Hkv, T, "2b", seed=44, append_block=2048, precision="vfast")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(45)
+    q = torch.randn(B, Hq, 128, device="cuda", generator=g)
+    out = cache.attend(q).cpu().numpy()
+    qn = q.cpu().numpy()
+    G = Hq // Hkv
+    worst = 0.0
+    for u in (0, (B * Hkv) // 2 + 3, B * Hkv - 1):
+        b, h = divmod(u, Hkv)
+        ref = _oracle_unit_out(cache, u, qn[b, h * G:(h + 1) * G])
+        got = out[b, h * G:(h + 1) * G]
+        for i in range(G):
+            err = np.max(np.abs(got[i] - ref[i])) / np.max(np.abs(ref[i]))
+            worst = max(worst, err)
+            assert err <= TOL, (u, i, err)
+    print(f"[C4 full size] worst max-rel error {worst:.2e}")
+    assert np.isfinite(out).all()
