@@ -44,14 +44,16 @@ def _wire_all(cache, kind):
     return pages_to_wire(cache.all_pages(kind), cache.bit_mode, cache.config.strategy, kind)
 
 
-@pytest.mark.parametrize("mode,dist", [("2b", "normal"), ("1b", "mis")])
-def test_encode_c3_scale_bit_exact_vs_oracle(mode, dist):
+@pytest.mark.parametrize("mode,dist,B,T", [("2b", "normal", 8, 16384), ("1b", "mis", 8, 16384),
+                                            # BASELINE config 3 at full size: 65,536 chunks per side
+                                            ("2b", "normal", 64, 8192), ("1b", "normal", 64, 8192)])
+def test_encode_c3_scale_bit_exact_vs_oracle(mode, dist, B, T):
     import torch
 
     import paper_2505_18231_b200 as P
     from oracle import oracle as orc
 
-    B, H, T = 8, 8, 16384  # 16,384 chunks per side
+    H = 8
     cb = P.default_codebook(mode)
     cfg = P.CacheConfig(d=128, bit_mode=cb.bit_mode)
     gen = torch.Generator(device="cuda")
